@@ -1,0 +1,465 @@
+// sf_api.cu -- host implementation of include/staleflow.h: context, device memory layout,
+// window launch sequence, transfers and dumps.  No simulation arithmetic runs on the host.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/staleflow.h"
+#include "sf_internal.cuh"
+
+using sf::Dev;
+using sf::GParams;
+using sf::ScenConst;
+using sf::ScenState;
+
+struct sf_ctx {
+  GParams P{};
+  Dev D{};
+  std::vector<ScenConst> hsc;
+  std::vector<int> hn_pool;
+  int n_inst_total = 0;
+  int n_scen = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<void *> allocs;
+  std::string err;
+  int poisoned = 0;
+  long long launches = 0;
+  long long *d_metrics = nullptr;
+  int *d_collect = nullptr;
+  int *d_stage = nullptr;
+  size_t stage_cap = 0;
+  long long *d_dump = nullptr;
+  size_t dump_cap = 0;
+};
+
+namespace {
+
+sf_status fail(sf_ctx *c, sf_status st, const std::string &msg) {
+  if (c) {
+    c->err = msg;
+    if (st == SF_E_STATE || st == SF_E_CUDA) c->poisoned = 1;
+  }
+  return st;
+}
+
+bool cuda_ok(sf_ctx *c, cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return true;
+  if (c) {
+    c->err = std::string(what) + ": " + cudaGetErrorString(e);
+    c->poisoned = 1;
+  }
+  return false;
+}
+
+template <typename T>
+bool dalloc(sf_ctx *c, T **p, long long count, int fill_byte) {
+  size_t bytes = (size_t)std::max<long long>(count, 1) * sizeof(T);
+  void *q = nullptr;
+  if (cudaMalloc(&q, bytes) != cudaSuccess) return false;
+  c->allocs.push_back(q);
+  if (cudaMemsetAsync(q, fill_byte, bytes, c->stream) != cudaSuccess) return false;
+  *p = (T *)q;
+  return true;
+}
+
+sf_status check_ctx(sf_ctx *c) {
+  if (!c) return SF_E_INVALID;
+  if (c->poisoned) return SF_E_STATE;
+  cudaSetDevice(c->device);
+  return SF_OK;
+}
+
+sf_status read_state(sf_ctx *c, int s, ScenState *out) {
+  if (!cuda_ok(c, cudaMemcpyAsync(out, c->D.ss + s, sizeof(ScenState), cudaMemcpyDeviceToHost, c->stream), "D2H state") ||
+      !cuda_ok(c, cudaStreamSynchronize(c->stream), "sync"))
+    return SF_E_CUDA;
+  return SF_OK;
+}
+
+sf_status reduce_metrics_host(sf_ctx *c, long long *out) {
+  sf_launch_reduce_metrics(c->D, c->n_scen, c->d_metrics, c->stream);
+  c->launches++;
+  if (!cuda_ok(c, cudaGetLastError(), "reduce launch") ||
+      !cuda_ok(c, cudaMemcpyAsync(out, c->d_metrics, sizeof(long long) * sf::kMetrics, cudaMemcpyDeviceToHost, c->stream),
+               "D2H metrics") ||
+      !cuda_ok(c, cudaStreamSynchronize(c->stream), "sync"))
+    return SF_E_CUDA;
+  return SF_OK;
+}
+
+sf_status check_errors(sf_ctx *c) {
+  // any poisoned scenario -> context poisoned
+  std::vector<ScenState> ss(c->n_scen);
+  if (!cuda_ok(c, cudaMemcpyAsync(ss.data(), c->D.ss, sizeof(ScenState) * c->n_scen, cudaMemcpyDeviceToHost, c->stream),
+               "D2H states") ||
+      !cuda_ok(c, cudaStreamSynchronize(c->stream), "sync"))
+    return SF_E_CUDA;
+  for (int s = 0; s < c->n_scen; ++s) {
+    if (ss[s].err) {
+      char buf[160];
+      snprintf(buf, sizeof buf, "scenario %d: invariant violated (code %d) at window %lld", s, ss[s].err, ss[s].window);
+      return fail(c, SF_E_STATE, buf);
+    }
+  }
+  return SF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf_config *cfg, sf_ctx **out) {
+  if (!cfg || !out || group_size < 1 || cfg->batch_size < 1 || cfg->n_scenarios < 1 || cfg->k5_tok < 1 ||
+      cfg->snap_period_ps <= 0 || cfg->pool_capacity_groups < 1 || cfg->kv_budget_tok < 1 ||
+      cfg->command_log_capacity < 0 || cfg->route_lat_ps < 0 || cfg->pull_lat_ps < 0 || cfg->reward_lat_ps < 0 ||
+      cfg->auto_train_windows < 0)
+    return SF_E_INVALID;
+  sf_ctx *c = new (std::nothrow) sf_ctx();
+  if (!c) return SF_E_NOMEM;
+  c->device = cfg->device;
+  if (cudaSetDevice(cfg->device) != cudaSuccess) { delete c; return SF_E_CUDA; }
+  c->stream = (cudaStream_t)cfg->cuda_stream;
+  const int ns = cfg->n_scenarios, B = cfg->batch_size, G = group_size;
+  GParams &P = c->P;
+  P.B = B; P.G = G;
+  P.k1 = cfg->k1_ps_per_tok; P.k2 = cfg->k2_ps; P.k3 = cfg->k3_ps; P.k4 = cfg->k4_ps;
+  P.k5 = cfg->k5_tok; P.kp = cfg->kprefill_ps_per_tok; P.M = cfg->kv_budget_tok;
+  P.mu = cfg->mu; P.phi_tp = cfg->phi_throughput; P.phi_wait = cfg->phi_wait;
+  P.delta = cfg->snap_period_ps; P.r = cfg->route_lat_ps; P.q = cfg->pull_lat_ps; P.R = cfg->reward_lat_ps;
+  P.atw = cfg->auto_train_windows; P.pool_cap = cfg->pool_capacity_groups;
+  P.cmdlog_cap = cfg->command_log_capacity; P.n_scen = ns;
+  c->n_scen = ns;
+  c->hsc.resize(ns);
+  c->hn_pool.assign(ns, 0);
+  long long inst = 0, led = 0, ring = 0, list = 0, bits = 0, mlq = 0, ev = 0, batch = 0, cmd = 0;
+  const long long pool_traj = (long long)P.pool_cap * G;
+  const long long bwords = (pool_traj + 31) / 32;
+  const long long batch_rec = (long long)(P.pool_cap / B + 1) * (1 + 2 * B);
+  for (int s = 0; s < ns; ++s) {
+    ScenConst &S = c->hsc[s];
+    S.I = cfg->scenario_instances ? cfg->scenario_instances[s] : instances;
+    S.eta = cfg->scenario_eta ? cfg->scenario_eta[s] : eta;
+    S.strategy = (int)(cfg->scenario_strategy ? cfg->scenario_strategy[s] : cfg->strategy);
+    if (S.I < 1 || S.I > sf::kMaxInst || S.eta < 0 || S.eta > sf::kMaxEta) {
+      delete c;
+      return SF_E_INVALID;
+    }
+    S.cap = (S.eta + 1) * B * G;
+    S.inst_off = (int)inst; S.grp_off = s * P.pool_cap; S.led_off = (int)led; S.ring_off = (int)ring;
+    S.traj_off = (long long)s * pool_traj; S.list_off = list; S.bits_off = bits; S.mlq_off = mlq;
+    S.ev_off = ev; S.batch_off = batch; S.cmd_off = cmd;
+    inst += S.I; led += (long long)(S.eta + 1) * B; ring += S.eta + 1; list += (long long)S.I * S.cap;
+    bits += bwords; mlq += 2LL * S.cap; ev += S.cap; batch += batch_rec; cmd += 4LL * P.cmdlog_cap;
+  }
+  c->n_inst_total = (int)inst;
+  const long long ntraj = (long long)ns * pool_traj, ngrp = (long long)ns * P.pool_cap;
+  Dev &D = c->D;
+  bool ok = true;
+  ScenConst *dsc = nullptr;
+  ScenState *dss = nullptr;
+  int *dinst_scen = nullptr;
+  ok = ok && dalloc(c, &dsc, ns, 0) && dalloc(c, &dss, ns, 0) && dalloc(c, &dinst_scen, inst, 0);
+  ok = ok && dalloc(c, &D.T, ntraj, 0) && dalloc(c, &D.gen, ntraj, 0) && dalloc(c, &D.loc, ntraj, 0) &&
+       dalloc(c, &D.tinst, ntraj, 0xFF) && dalloc(c, &D.n_routes, ntraj, 0) && dalloc(c, &D.n_preempt, ntraj, 0) &&
+       dalloc(c, &D.n_interrupt, ntraj, 0) && dalloc(c, &D.t_complete, ntraj, 0xFF) && dalloc(c, &D.ready, ntraj, 0);
+  ok = ok && dalloc(c, &D.prompt, ngrp, 0) && dalloc(c, &D.gv, ngrp, 0xFF) && dalloc(c, &D.n_rew, ngrp, 0) &&
+       dalloc(c, &D.led_b, ngrp, 0xFF) && dalloc(c, &D.led_s, ngrp, 0xFF) && dalloc(c, &D.cvbuf, ngrp, 0xFF);
+  ok = ok && dalloc(c, &D.iv, inst, 0) && dalloc(c, &D.ic, inst, 0) && dalloc(c, &D.ist, inst, 0) &&
+       dalloc(c, &D.ipullv, inst, 0) && dalloc(c, &D.ipullpend, inst, 0) && dalloc(c, &D.iintkind, inst, 0) &&
+       dalloc(c, &D.iintk, inst, 0) && dalloc(c, &D.irun_n, inst, 0) && dalloc(c, &D.iwhead, inst, 0) &&
+       dalloc(c, &D.iwn, inst, 0) && dalloc(c, &D.iarr_n, inst, 0) && dalloc(c, &D.ipv, inst, 0) &&
+       dalloc(c, &D.iacc, inst, 0) && dalloc(c, &D.ikv, inst, 0) && dalloc(c, &D.inb, inst, 0) &&
+       dalloc(c, &D.iuntil, inst, 0) && dalloc(c, &D.iprefill, inst, 0);
+  ok = ok && dalloc(c, &D.run_id, list, 0) && dalloc(c, &D.run_rem, list, 0) && dalloc(c, &D.wait_id, list, 0) &&
+       dalloc(c, &D.arr_id, list, 0) && dalloc(c, &D.arr_t, list, 0);
+  ok = ok && dalloc(c, &D.led_st, led, 0) && dalloc(c, &D.led_g, led, 0xFF) && dalloc(c, &D.led_v, led, 0xFF) &&
+       dalloc(c, &D.led_nres, ring, 0) && dalloc(c, &D.led_nocc, ring, 0);
+  ok = ok && dalloc(c, &D.ev_t, 1, 0) && dalloc(c, &D.ev_id, ev, 0) && dalloc(c, &D.tsv_bits, bits, 0) &&
+       dalloc(c, &D.mlq, mlq, 0) && dalloc(c, &D.batches, batch, 0) && dalloc(c, &D.cmdlog, cmd, 0);
+  ok = ok && dalloc(c, &c->d_metrics, sf::kMetrics, 0) && dalloc(c, &c->d_collect, 2 + 2 * B, 0);
+  if (!ok) {
+    sf_destroy(c);
+    return SF_E_NOMEM;
+  }
+  D.sc = dsc;
+  D.ss = dss;
+  D.inst_scen = dinst_scen;
+  std::vector<int> hinst_scen(inst);
+  for (int s = 0; s < ns; ++s)
+    for (int i = 0; i < c->hsc[s].I; ++i) hinst_scen[c->hsc[s].inst_off + i] = s;
+  std::vector<ScenState> hss(ns);
+  std::memset(hss.data(), 0, sizeof(ScenState) * ns);
+  for (int s = 0; s < ns; ++s) hss[s].cmd_hash = 1469598103934665603ULL;   // FNV-1a offset (§3.4)
+  bool cp = cudaMemcpyAsync(dsc, c->hsc.data(), sizeof(ScenConst) * ns, cudaMemcpyHostToDevice, c->stream) == cudaSuccess &&
+            cudaMemcpyAsync(dss, hss.data(), sizeof(ScenState) * ns, cudaMemcpyHostToDevice, c->stream) == cudaSuccess &&
+            cudaMemcpyAsync(dinst_scen, hinst_scen.data(), sizeof(int) * inst, cudaMemcpyHostToDevice, c->stream) == cudaSuccess &&
+            cudaStreamSynchronize(c->stream) == cudaSuccess;
+  if (!cp) {
+    sf_destroy(c);
+    return SF_E_CUDA;
+  }
+  *out = c;
+  return SF_OK;
+}
+
+void sf_destroy(sf_ctx *c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  else cudaDeviceSynchronize();
+  for (void *p : c->allocs) cudaFree(p);
+  if (c->d_stage) cudaFree(c->d_stage);
+  if (c->d_dump) cudaFree(c->d_dump);
+  delete c;
+}
+
+sf_status sf_submit_prompts_many(sf_ctx *c, int32_t n, const int32_t *scen_ids, const int32_t *n_groups,
+                                 const int32_t *prompt, const int32_t *target) {
+  sf_status st = check_ctx(c);
+  if (st != SF_OK) return st;
+  if (n < 0 || (n > 0 && (!scen_ids || !n_groups || !prompt || !target))) return fail(c, SF_E_INVALID, "null argument");
+  const int G = c->P.G;
+  std::vector<int> desc;
+  std::vector<int> pool = c->hn_pool;
+  long long tot = 0;
+  for (int k = 0; k < n; ++k) {
+    const int s = scen_ids[k], ng = n_groups[k];
+    if (s < 0 || s >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
+    if (ng < 0 || pool[s] + ng > c->P.pool_cap) return fail(c, SF_E_RANGE, "pool capacity exceeded");
+    for (long long a = 0; a < ng; ++a) {
+      const long long p = prompt[tot + a];
+      if (p < 0) return fail(c, SF_E_INVALID, "negative prompt length");
+      for (int m = 0; m < G; ++m) {
+        const long long T = target[(tot + a) * G + m];
+        if (T < 1 || (long long)c->P.k5 * (p + T) > c->P.M) return fail(c, SF_E_INVALID, "target < 1 or k5*(p+T) > M (A27)");
+      }
+    }
+    desc.push_back(s); desc.push_back(pool[s]); desc.push_back(ng); desc.push_back((int)tot);
+    pool[s] += ng;
+    tot += ng;
+  }
+  if (tot == 0) return SF_OK;
+  const size_t need = (size_t)desc.size() + (size_t)tot + (size_t)tot * G;
+  if (need > c->stage_cap) {
+    if (c->d_stage) cudaFree(c->d_stage);
+    c->d_stage = nullptr;
+    if (cudaMalloc(&c->d_stage, need * sizeof(int)) != cudaSuccess) return fail(c, SF_E_NOMEM, "staging alloc");
+    c->stage_cap = need;
+  }
+  int *ddesc = c->d_stage, *dp = c->d_stage + desc.size(), *dt = dp + tot;
+  if (!cuda_ok(c, cudaMemcpyAsync(ddesc, desc.data(), desc.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream), "H2D desc") ||
+      !cuda_ok(c, cudaMemcpyAsync(dp, prompt, tot * sizeof(int), cudaMemcpyHostToDevice, c->stream), "H2D prompts") ||
+      !cuda_ok(c, cudaMemcpyAsync(dt, target, tot * G * sizeof(int), cudaMemcpyHostToDevice, c->stream), "H2D targets"))
+    return SF_E_CUDA;
+  sf_launch_scatter_pool(c->D, G, ddesc, n, dp, dt, c->stream);
+  c->launches++;
+  if (!cuda_ok(c, cudaGetLastError(), "scatter launch") || !cuda_ok(c, cudaStreamSynchronize(c->stream), "sync"))
+    return SF_E_CUDA;
+  c->hn_pool = pool;
+  return SF_OK;
+}
+
+sf_status sf_submit_prompts(sf_ctx *c, int32_t scenario, int32_t n_groups, const int32_t *prompt_len,
+                            const int32_t *target_len) {
+  return sf_submit_prompts_many(c, 1, &scenario, &n_groups, prompt_len, target_len);
+}
+
+sf_status sf_step(sf_ctx *c, int32_t n_windows, sf_step_stats *out) {
+  sf_status st = check_ctx(c);
+  if (st != SF_OK) return st;
+  if (n_windows < 0) return fail(c, SF_E_INVALID, "n_windows < 0");
+  long long before[sf::kMetrics] = {0}, after[sf::kMetrics] = {0};
+  if (out && (st = reduce_metrics_host(c, before)) != SF_OK) return st;
+  for (int w = 0; w < n_windows; ++w) {
+    sf_launch_begin_coord(c->P, c->D, c->n_scen, c->stream);
+    sf_launch_advance(c->P, c->D, c->n_inst_total, c->stream);
+    sf_launch_ledger(c->P, c->D, c->n_scen, c->stream);
+    c->launches += 3;
+  }
+  if (!cuda_ok(c, cudaGetLastError(), "window launch")) return SF_E_CUDA;
+  if (out) {
+    if ((st = reduce_metrics_host(c, after)) != SF_OK) return st;
+    if ((st = check_errors(c)) != SF_OK) return st;
+    out->windows = after[sf::M_WINDOWS] - before[sf::M_WINDOWS];
+    out->ticks = after[sf::M_TICKS] - before[sf::M_TICKS];
+    out->traj_iters = after[sf::M_TRAJ_ITERS] - before[sf::M_TRAJ_ITERS];
+    out->tokens = after[sf::M_TOKENS] - before[sf::M_TOKENS];
+    out->completions = after[sf::M_COMPLETIONS] - before[sf::M_COMPLETIONS];
+    out->routes = after[sf::M_ROUTES] - before[sf::M_ROUTES];
+    out->interrupts = after[sf::M_INTERRUPTS] - before[sf::M_INTERRUPTS];
+    out->pulls = after[sf::M_PULLS] - before[sf::M_PULLS];
+    out->preemptions = after[sf::M_PREEMPTIONS] - before[sf::M_PREEMPTIONS];
+    out->batches = after[sf::M_BATCHES] - before[sf::M_BATCHES];
+    out->invalid_snapshots = after[sf::M_INVALID_SNAP] - before[sf::M_INVALID_SNAP];
+    out->violations = after[sf::M_VIOLATIONS] - before[sf::M_VIOLATIONS];
+    ScenState s0;
+    if ((st = read_state(c, 0, &s0)) != SF_OK) return st;
+    out->sim_time_ps = s0.t;
+  }
+  return SF_OK;
+}
+
+sf_status sf_publish_params(sf_ctx *c, int32_t scenario, int32_t v) {
+  sf_status st = check_ctx(c);
+  if (st != SF_OK) return st;
+  if (scenario < 0 || scenario >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
+  ScenState s;
+  if ((st = read_state(c, scenario, &s)) != SF_OK) return st;
+  if (v != s.ps + 1 || v > s.cu) return fail(c, SF_E_VERSION, "publish: version must be ps+1 and <= consumed batches");
+  s.ps = v;
+  s.m[sf::M_PUBLISHES] += 1;
+  if (!cuda_ok(c, cudaMemcpyAsync(&c->D.ss[scenario].ps, &s.ps, sizeof(int), cudaMemcpyHostToDevice, c->stream), "H2D ps") ||
+      !cuda_ok(c, cudaMemcpyAsync(&c->D.ss[scenario].m[sf::M_PUBLISHES], &s.m[sf::M_PUBLISHES], sizeof(unsigned long long),
+                                  cudaMemcpyHostToDevice, c->stream), "H2D m") ||
+      !cuda_ok(c, cudaStreamSynchronize(c->stream), "sync"))
+    return SF_E_CUDA;
+  return SF_OK;
+}
+
+sf_status sf_collect_batch(sf_ctx *c, int32_t scenario, int32_t cap, int32_t *v_buf, int32_t *group_ids,
+                           int32_t *group_versions, int32_t *n_out) {
+  sf_status st = check_ctx(c);
+  if (st != SF_OK) return st;
+  if (scenario < 0 || scenario >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
+  const int B = c->P.B;
+  if (n_out) *n_out = B;
+  if (cap < B) return fail(c, SF_E_RANGE, "collect: cap < batch_size");
+  sf_launch_collect(c->P, c->D, scenario, c->d_collect, c->stream);
+  c->launches++;
+  std::vector<int> h(2 + 2 * B);
+  if (!cuda_ok(c, cudaGetLastError(), "collect launch") ||
+      !cuda_ok(c, cudaMemcpyAsync(h.data(), c->d_collect, h.size() * sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H") ||
+      !cuda_ok(c, cudaStreamSynchronize(c->stream), "sync"))
+    return SF_E_CUDA;
+  if (h[0] != 0) return SF_NOT_READY;
+  if (v_buf) *v_buf = h[1];
+  for (int k = 0; k < B; ++k) {
+    if (group_ids) group_ids[k] = h[2 + 2 * k];
+    if (group_versions) group_versions[k] = h[3 + 2 * k];
+  }
+  return check_errors(c);
+}
+
+sf_status sf_read_metrics(sf_ctx *c, int64_t *out, int32_t len) {
+  sf_status st = check_ctx(c);
+  if (st != SF_OK) return st;
+  if (!out || len < 0) return fail(c, SF_E_INVALID, "bad output");
+  long long m[sf::kMetrics];
+  if ((st = reduce_metrics_host(c, m)) != SF_OK) return st;
+  for (int k = 0; k < len; ++k) out[k] = k < sf::kMetrics ? m[k] : 0;
+  return SF_OK;
+}
+
+sf_status sf_read_metrics_device(sf_ctx *c, int64_t *out_dev) {
+  sf_status st = check_ctx(c);
+  if (st != SF_OK) return st;
+  if (!out_dev) return fail(c, SF_E_INVALID, "null output");
+  sf_launch_reduce_metrics(c->D, c->n_scen, (long long *)out_dev, c->stream);
+  c->launches++;
+  return cuda_ok(c, cudaGetLastError(), "reduce launch") ? SF_OK : SF_E_CUDA;
+}
+
+sf_status sf_read_scenario_metrics(sf_ctx *c, int32_t scenario, int64_t *out, int32_t len) {
+  sf_status st = check_ctx(c);
+  if (st != SF_OK) return st;
+  if (scenario < 0 || scenario >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
+  ScenState s;
+  if ((st = read_state(c, scenario, &s)) != SF_OK) return st;
+  for (int k = 0; k < len; ++k) {
+    long long v = k < sf::kMetrics ? (long long)s.m[k] : 0;
+    if (k == sf::M_CMD_HASH) v = (long long)s.cmd_hash;
+    if (k == sf::M_SIM_TIME) v = s.t;
+    out[k] = v;
+  }
+  return SF_OK;
+}
+
+static sf_status ensure_dump(sf_ctx *c, size_t n) {
+  if (n <= c->dump_cap) return SF_OK;
+  if (c->d_dump) cudaFree(c->d_dump);
+  c->d_dump = nullptr;
+  if (cudaMalloc(&c->d_dump, n * sizeof(long long)) != cudaSuccess) return fail(c, SF_E_NOMEM, "dump alloc");
+  c->dump_cap = n;
+  return SF_OK;
+}
+
+sf_status sf_dump_lifecycles(sf_ctx *c, int32_t scenario, int64_t *rec, int64_t cap, int64_t *n) {
+  sf_status st = check_ctx(c);
+  if (st != SF_OK) return st;
+  if (scenario < 0 || scenario >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
+  const long long cnt = (long long)c->hn_pool[scenario] * c->P.G;
+  if (n) *n = cnt;
+  if (cap < cnt || (cnt > 0 && !rec)) return SF_E_RANGE;
+  if (cnt == 0) return SF_OK;
+  if ((st = ensure_dump(c, 13 * cnt)) != SF_OK) return st;
+  sf_launch_dump_lifecycles(c->P, c->D, scenario, cnt, c->d_dump, c->stream);
+  c->launches += 2;
+  if (!cuda_ok(c, cudaGetLastError(), "dump launch") ||
+      !cuda_ok(c, cudaMemcpyAsync(rec, c->d_dump, 13 * cnt * sizeof(long long), cudaMemcpyDeviceToHost, c->stream), "D2H") ||
+      !cuda_ok(c, cudaStreamSynchronize(c->stream), "sync"))
+    return SF_E_CUDA;
+  return SF_OK;
+}
+
+sf_status sf_dump_batches(sf_ctx *c, int32_t scenario, int32_t *out, int64_t cap, int64_t *n) {
+  sf_status st = check_ctx(c);
+  if (st != SF_OK) return st;
+  if (scenario < 0 || scenario >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
+  ScenState s;
+  if ((st = read_state(c, scenario, &s)) != SF_OK) return st;
+  const long long cnt = (long long)s.batch_n * (1 + 2 * c->P.B);
+  if (n) *n = cnt;
+  if (cap < cnt || (cnt > 0 && !out)) return SF_E_RANGE;
+  if (cnt == 0) return SF_OK;
+  if (!cuda_ok(c, cudaMemcpyAsync(out, c->D.batches + c->hsc[scenario].batch_off, cnt * sizeof(int), cudaMemcpyDeviceToHost,
+                                  c->stream), "D2H") ||
+      !cuda_ok(c, cudaStreamSynchronize(c->stream), "sync"))
+    return SF_E_CUDA;
+  return SF_OK;
+}
+
+sf_status sf_dump_commands(sf_ctx *c, int32_t scenario, int64_t *rec, int64_t cap, int64_t *n) {
+  sf_status st = check_ctx(c);
+  if (st != SF_OK) return st;
+  if (scenario < 0 || scenario >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
+  ScenState s;
+  if ((st = read_state(c, scenario, &s)) != SF_OK) return st;
+  const long long cnt = std::min<long long>(s.cmd_n, c->P.cmdlog_cap);
+  if (n) *n = cnt;
+  if (cap < cnt || (cnt > 0 && !rec)) return SF_E_RANGE;
+  if (cnt == 0) return SF_OK;
+  if (!cuda_ok(c, cudaMemcpyAsync(rec, c->D.cmdlog + c->hsc[scenario].cmd_off, 4 * cnt * sizeof(long long),
+                                  cudaMemcpyDeviceToHost, c->stream), "D2H") ||
+      !cuda_ok(c, cudaStreamSynchronize(c->stream), "sync"))
+    return SF_E_CUDA;
+  return SF_OK;
+}
+
+sf_status sf_dump_instances(sf_ctx *c, int32_t scenario, int64_t *out, int64_t cap, int64_t *n) {
+  sf_status st = check_ctx(c);
+  if (st != SF_OK) return st;
+  if (scenario < 0 || scenario >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
+  const int I = c->hsc[scenario].I;
+  if (n) *n = I;
+  if (cap < I || !out) return SF_E_RANGE;
+  if ((st = ensure_dump(c, 7 * (size_t)I)) != SF_OK) return st;
+  sf_launch_dump_instances(c->P, c->D, scenario, c->d_dump, c->stream);
+  c->launches++;
+  if (!cuda_ok(c, cudaGetLastError(), "dump launch") ||
+      !cuda_ok(c, cudaMemcpyAsync(out, c->d_dump, 7 * I * sizeof(long long), cudaMemcpyDeviceToHost, c->stream), "D2H") ||
+      !cuda_ok(c, cudaStreamSynchronize(c->stream), "sync"))
+    return SF_E_CUDA;
+  return SF_OK;
+}
+
+int64_t sf_kernel_launches(const sf_ctx *c) { return c ? c->launches : 0; }
+
+const char *sf_last_error(const sf_ctx *c) { return c ? c->err.c_str() : "null context"; }
+
+}  // extern "C"
