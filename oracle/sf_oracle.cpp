@@ -316,7 +316,7 @@ struct Inst {
   int v = 0; int64_t kv = 0; std::vector<int> run; std::deque<int> wait; int c = 0;
   int st = I_IDLE; int64_t nb = 0, pull_until = 0; int pull_version = 0;
   bool pull_pending = false, cmd_at_t = false;
-  std::vector<int> interrupt_set;
+  std::vector<std::pair<int, int64_t>> interrupt_set;   // (trajectory, context held here at issue)
   std::vector<Arrival> arrivals;
   int64_t prefill = 0;
   int pv = 0, acc = 0;                   // speculative state P[i], initialised to 0
@@ -395,7 +395,7 @@ void coordinate(Scen &s) {
   auto interrupt = [&](int i, const std::vector<int> &victims) {
     for (int j : victims) {
       log_cmd(s, CMD_INTERRUPT, i, j);
-      s.inst[i].interrupt_set.push_back(j);
+      s.inst[i].interrupt_set.push_back({j, (int64_t)ctx_len(s, j)});
       s.traj[j].st = L_TS;
       s.traj[j].ready = apply_time(i);
       s.traj[j].n_interrupt++;
@@ -469,9 +469,12 @@ void boundary(Scen &s, int i, int64_t b) {
   n.cmd_at_t = false;
   // B1: pending interrupts leave run/wait without this tick's token; their KV is released.
   if (n.st != I_PULL && !n.interrupt_set.empty()) {
-    for (int j : n.interrupt_set) {
+    // The KV released is the context this instance holds (A17): the trajectory's progress is
+    // frozen here since issue, while it may already be running elsewhere after re-routing.
+    for (const auto &jc : n.interrupt_set) {
+      const int j = jc.first;
       auto it = std::find(n.run.begin(), n.run.end(), j);
-      if (it != n.run.end()) { n.kv -= (int64_t)P.k5 * ctx_len(s, j); n.run.erase(it); continue; }
+      if (it != n.run.end()) { n.kv -= (int64_t)P.k5 * jc.second; n.run.erase(it); continue; }
       auto jt = std::find(n.wait.begin(), n.wait.end(), j);
       if (jt != n.wait.end()) { n.wait.erase(jt); continue; }
       s.err = SFO_E_STATE;
@@ -535,6 +538,12 @@ void boundary(Scen &s, int i, int64_t b) {
     n.kv += (int64_t)P.k5 * ctx;
     n.prefill += ctx;
     s.traj[j].st = L_RUN;
+  }
+  // Invariant: kv = k5 x sum of the contexts of the running trajectories.
+  {
+    int64_t sum = 0;
+    for (int j : n.run) sum += (int64_t)P.k5 * ctx_len(s, j);
+    if (sum != n.kv || n.kv > P.M) s.err = SFO_E_STATE;
   }
   // B8: start the next decode step (Eq 7 + prefill stall, A20).
   if (!n.run.empty()) {
