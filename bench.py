@@ -1,0 +1,363 @@
+#!/usr/bin/env python
+"""bench.py -- StaleFlow coordination step (arXiv 2601.12784) on B200.
+
+Metric (BASELINE.json): trajectory-iterations per second (one running trajectory advanced by
+one decode step of its instance) and the advance kernel's HBM roofline fraction.
+
+Workload: the C5 configuration -- independent coordination scenarios (4 instances, B = 64,
+G = 8, eta 0..3, lognormal lengths sigma 0.25..1.5, full SF strategies) -- 4096 scenarios per
+GPU, weak scaling (rank r runs scenarios [r*4096, (r+1)*4096) of the same seeded family).  A
+"step" is one sf_step window (W0-W9 of DESIGN.md §3.1) over every scenario on the GPU, i.e.
+one pass of all of §8(a)'s rows.  L2 is flushed (512 MiB write) between timed windows.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU, NCCL)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "trajectory-iterations/sec per GPU and HBM GB/s fraction at 1/2/4/8 B200"
+UNIT = "trajectory-iterations/s"
+ALGO_BYTES_PER_ITER = 8          # read + write of the int32 remaining-length counter
+FALLBACK_HBM_GBS = 6650.0        # B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="staleflow", choices=["staleflow", "reference"])
+    ap.add_argument("--scenarios", type=int, default=4096, help="scenarios per GPU (C5 family)")
+    ap.add_argument("--flush-mb", type=int, default=512)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--profile-run", action="store_true", help="short run for ncu (no e2e / cpu legs)")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", d
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)", {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows if len(r) >= 9 for k in range(4) if r[5 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def scenario_slice(p, rank, per_gpu):
+    from paper_2601_12784_b200 import workload as W
+    idx = list(range(rank * per_gpu, (rank + 1) * per_gpu))
+    return W.preset_scenario_slice(p, idx), idx
+
+
+def pool_arrays(p, idx, n_groups, group0=0):
+    import numpy as np
+    from paper_2601_12784_b200 import workload as W
+    prs, tgs = [], []
+    for k in idx:
+        pr, tg = W.draw_lengths(p, k, n_groups, group0)
+        prs.append(pr)
+        tgs.append(tg)
+    return np.concatenate(prs), np.concatenate(tgs)
+
+
+# ------------------------------------------------------------------------------ reference arm
+def run_reference(args, rank, world):
+    """The oracle, as it stands, on the host cores: same metric/config, bounded sample."""
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle.oracle import OracleSim
+    from paper_2601_12784_b200 import workload as W
+    full = W.preset("C5", n_scenarios=args.scenarios)
+    n_sample = min(32, args.scenarios)
+    idx = list(range(n_sample))
+    o = OracleSim.from_preset(full, idx)
+    for a, k in enumerate(idx):
+        pr, tg = W.draw_lengths(full, k, full.pool_groups)
+        assert o.submit(a, pr, tg) == 0
+    cores = os.cpu_count() or 1
+    o.step(args.warmup, cores)
+    m0 = o.metrics()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        o.step(1, cores)
+    dt = time.perf_counter() - t0
+    it = int(o.metrics()[2] - m0[2])
+    v = it / dt
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+           "config": {"workload": f"C5 (sample of {n_sample} of {args.scenarios} scenarios/GPU)",
+                      "scenarios_per_step": n_sample, "windows_per_step": 1},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                            "sample": f"{n_sample} C5 scenarios x {args.steps} windows after {args.warmup} warm-up"},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------------------ cpu baseline
+def cpu_baseline(full, idx_all, warmup, target_s):
+    from oracle.oracle import OracleSim
+    from paper_2601_12784_b200 import workload as W
+    cores = os.cpu_count() or 1
+    n_sample = min(64, len(idx_all))
+    idx = idx_all[:n_sample]
+    o = OracleSim.from_preset(full, idx)
+    for a, k in enumerate(idx):
+        pr, tg = W.draw_lengths(full, k, full.pool_groups)
+        assert o.submit(a, pr, tg) == 0
+    o.step(warmup, cores)
+    m0 = o.metrics()
+    t0 = time.perf_counter()
+    windows = 0
+    while time.perf_counter() - t0 < target_s and windows < 400:
+        o.step(1, cores)
+        windows += 1
+    dt = time.perf_counter() - t0
+    it = int(o.metrics()[2] - m0[2])
+    return {"value": it / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{n_sample} C5 scenarios x {windows} windows after {warmup} warm-up ({dt:.1f} s)"}
+
+
+# ------------------------------------------------------------------------------ main arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2601_12784_b200 import workload as W
+    from paper_2601_12784_b200.staleflow import StaleFlow
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    S = args.scenarios
+    full = W.preset("C5", n_scenarios=S * world)
+    p, idx = scenario_slice(full, rank, S)
+    ctx = StaleFlow.from_preset(p, stream=stream)
+    pr, tg = pool_arrays(full, idx, full.pool_groups)
+    assert ctx.submit_many(np.arange(S), np.full(S, full.pool_groups), pr, tg) == 0
+    flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    ctx.step(args.warmup)
+    barrier()
+    m0 = ctx.metrics()
+    l0 = ctx.kernel_launches
+    clocks = ClockSampler(local)
+    clocks.start()
+    ctx.profile(True)
+    evs = []
+    barrier()
+    for _ in range(args.steps):
+        flush.zero_()                                   # L2 flush, outside the timed events
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        ctx.step(1)
+        e.record(stream)
+        evs.append((s, e))
+    barrier()
+    ms = sum(s.elapsed_time(e) for s, e in evs)
+    ctx.profile(False)
+    kern_ms, kern_n = ctx.profile_read()
+    clk = clocks.stop()
+    m1 = ctx.metrics()
+    launches = ctx.kernel_launches - l0 - 1             # minus the metrics reduction at m1
+    local_iters = int(m1[2] - m0[2])
+    dm = torch.tensor((m1 - m0).astype(np.int64), device="cuda")
+    tm = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    adv = torch.tensor([kern_ms[1]], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(dm, op=dist.ReduceOp.SUM)        # the metrics all-reduce (NCCL over NVLink)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        dist.all_reduce(adv, op=dist.ReduceOp.MAX)
+    total_iters = int(dm[2].item())
+    max_ms = float(tm.item())
+    value = total_iters / (max_ms / 1e3)
+
+    # ---------------- roofline of the dominant kernel (k_advance) from the live CUDA events
+    hbm, peak_src, _ = peaks()
+    adv_ms_per_launch = kern_ms[1] / max(1, kern_n[1])
+    bytes_per_launch = ALGO_BYTES_PER_ITER * local_iters / max(1, kern_n[1])
+    achieved = bytes_per_launch / (adv_ms_per_launch / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_advance_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    share = {k: kern_ms[i] / max(1e-9, kern_ms[:3].sum()) for i, k in enumerate(("coordinate", "advance", "ledger"))}
+
+    # ---------------- e2e: the same metric through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e and not args.profile_run:
+        e2e = run_e2e(args, full, idx, stream, world, barrier)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu and not args.profile_run:
+        cpu = cpu_baseline(full, idx, args.warmup, args.cpu_seconds)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": "C5: independent coordination scenarios (I=4, B=64, G=8, eta 0..3, "
+                                   "lognormal skew 0.25..1.5, SF R/S/M), 1 step = 1 window over all",
+                       "scenarios_per_gpu": S, "global_scenarios": S * world, "windows_per_step": 1,
+                       "parallelism": f"scenario-sharded x{world}", "l2": f"flushed ({args.flush_mb} MiB write) "
+                                                                          "between timed windows"},
+            "roofline": {"bound": "hbm", "kernel": "k_advance", "achieved": achieved, "peak": hbm,
+                         "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                         "algorithmic_bytes_per_traj_iter": ALGO_BYTES_PER_ITER,
+                         "launches": int(kern_n[1]), "ms_per_launch": adv_ms_per_launch,
+                         "step_share": share},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "sim": {"routes": int(dm[5].item()), "completions": int(dm[4].item()), "batches": int(dm[9].item()),
+                    "interrupts": int(dm[6].item()), "pulls": int(dm[7].item()),
+                    "invalid_snapshots": int(dm[11].item()), "violations": int(dm[12].item())},
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, full, idx, stream, world, barrier):
+    """Per step: H2D of that window's new prompts from pinned host memory through
+    sf_submit_prompts_many, sf_step (one window), D2H of the step's metric deltas."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2601_12784_b200 import workload as W
+    from paper_2601_12784_b200.staleflow import StaleFlow
+    S = len(idx)
+    p = W.preset_scenario_slice(full, idx)
+    ctx = StaleFlow.from_preset(p, stream=stream)
+    B = full.batch_size
+    eta_max = max(s.eta for s in p.scenarios)
+    first = (eta_max + 1) * B                              # the initial TS fill
+    per_step = B // 8                                      # 8 groups/scenario/window keeps the TS fed
+    total_windows = args.warmup + args.steps
+    pool = full.pool_groups
+    ctx_first = pool_arrays(full, idx, first)
+    assert ctx.submit_many(np.arange(S), np.full(S, first), *ctx_first) == 0
+    submitted = first
+    chunks = []
+    for w in range(total_windows):
+        ng = min(per_step, pool - submitted)
+        if ng <= 0:
+            chunks.append(None)
+            continue
+        pr, tg = pool_arrays(full, idx, ng, submitted)
+        hp = [torch.from_numpy(np.arange(S, dtype=np.int32)).pin_memory(),
+              torch.from_numpy(np.full(S, ng, np.int32)).pin_memory(),
+              torch.from_numpy(pr).pin_memory(), torch.from_numpy(tg).pin_memory()]
+        chunks.append((ng, hp))
+        submitted += ng
+    iters = 0
+    h2d = d2h = 0
+    t_total = 0.0
+    for w in range(total_windows):
+        timed = w >= args.warmup
+        if timed and w == args.warmup:
+            barrier()
+        t0 = time.perf_counter()
+        if chunks[w] is not None:
+            ng, hp = chunks[w]
+            assert ctx.submit_many_ptr(S, *(x.data_ptr() for x in hp)) == 0
+            if timed:
+                h2d += sum(x.numel() * 4 for x in hp)
+        st = ctx.step(1, stats=True)                       # syncs + D2H of the metric deltas
+        t1 = time.perf_counter()
+        if timed:
+            t_total += t1 - t0
+            iters += st["traj_iters"]
+            d2h += 2 * 32 * 8
+    tt = torch.tensor([t_total], dtype=torch.float64, device="cuda")
+    it = torch.tensor([iters], dtype=torch.int64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dist.all_reduce(it, op=dist.ReduceOp.SUM)
+    ctx.close()
+    return {"value": int(it.item()) / float(tt.item()), "unit": UNIT,
+            "h2d_bytes_per_step": h2d // max(1, args.steps), "d2h_bytes_per_step": d2h // max(1, args.steps),
+            "note": "per window: pinned H2D of new prompts (sf_submit_prompts_many), sf_step, D2H of metrics; "
+                    "host wall clock, max over ranks"}
+
+
+if __name__ == "__main__":
+    main()

@@ -111,7 +111,8 @@ sf_status sf_publish_params(sf_ctx *ctx, int32_t scenario, int32_t new_version);
 sf_status sf_collect_batch(sf_ctx *ctx, int32_t scenario, int32_t cap, int32_t *v_buf, int32_t *group_ids,
                            int32_t *group_versions, int32_t *n_out);
 
-/* Cumulative int64 metrics summed over scenarios into host out[len]. */
+/* Cumulative int64 metrics summed over scenarios into host out[len]; slot 29
+ * counts poisoned scenarios and slot 30 is the maximum simulated time. */
 sf_status sf_read_metrics(sf_ctx *ctx, int64_t *out, int32_t len);
 /* Same, written to DEVICE memory out_dev[SF_METRICS_LEN] on the context stream (no sync);
  * this is the NCCL all-reduce payload. */
@@ -134,6 +135,13 @@ sf_status sf_dump_instances(sf_ctx *ctx, int32_t scenario, int64_t *out, int64_t
 
 /* Number of kernels this context has launched so far. */
 int64_t sf_kernel_launches(const sf_ctx *ctx);
+
+/* Live per-kernel timing: while enabled, sf_step records CUDA events on the context stream
+ * around each window kernel (0 coordinate, 1 advance, 2 ledger).  sf_profile_read synchronizes
+ * the stream and returns (then resets) the accumulated milliseconds and launch counts in
+ * ms[len] / launches[len] (len <= 4). */
+sf_status sf_profile(sf_ctx *ctx, int32_t enable);
+sf_status sf_profile_read(sf_ctx *ctx, double *ms, int64_t *launches, int32_t len);
 
 /* Message for the last failing call; owned by the context, valid until the next call. */
 const char *sf_last_error(const sf_ctx *ctx);

@@ -23,7 +23,7 @@ METRIC_NAMES = [
     "preemptions", "batches", "valid_snapshots", "invalid_snapshots", "violations", "publishes",
     "ingested_groups", "occupied_groups",
     "stale_0", "stale_1", "stale_2", "stale_3", "stale_4", "stale_5", "stale_6", "stale_7", "stale_8+",
-    "command_hash", "sim_time_ps", "reserves", "relocations", "rsv29", "rsv30", "rsv31",
+    "command_hash", "sim_time_ps", "reserves", "relocations", "poisoned_scenarios", "max_sim_time_ps", "rsv31",
 ]
 
 _lock = threading.Lock()

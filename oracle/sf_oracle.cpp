@@ -751,7 +751,8 @@ int sfo_read_scenario_metrics(sfo_sim *sim, int32_t k, int64_t *out, int32_t len
   for (int a = 0; a < len && a < SFO_METRICS_LEN; ++a) {
     int64_t v = s.m[a];
     if (a == M_CMD_HASH) v = (int64_t)s.cmd_hash;
-    if (a == M_SIM_TIME) v = s.t;
+    if (a == M_SIM_TIME || a == 30) v = s.t;       // slot 30: max simulated time (per scenario: t)
+    if (a == 29) v = s.err != 0;                   // slot 29: poisoned scenarios
     out[a] = v;
   }
   return SFO_OK;
@@ -764,7 +765,7 @@ int sfo_read_metrics(sfo_sim *sim, int64_t *out, int32_t len) {
   for (int k = 0; k < (int)sim->sc.size(); ++k) {
     sfo_read_scenario_metrics(sim, k, tmp, SFO_METRICS_LEN);
     for (int a = 0; a < len && a < SFO_METRICS_LEN; ++a)
-      out[a] = (int64_t)((uint64_t)out[a] + (uint64_t)tmp[a]);
+      out[a] = a == 30 ? std::max(out[a], tmp[a]) : (int64_t)((uint64_t)out[a] + (uint64_t)tmp[a]);
   }
   return SFO_OK;
 }

@@ -195,7 +195,9 @@ __global__ void k_reduce_metrics(Dev D, int n_scen, long long *out) {
     unsigned long long v = SS.m[k];
     if (k == M_CMD_HASH) v = SS.cmd_hash;
     if (k == M_SIM_TIME) v = (unsigned long long)SS.t;
-    atomicAdd(&acc[k], v);
+    if (k == M_ERR_SCEN) v = SS.err != 0;
+    if (k == M_MAX_T) atomicMax(&acc[k], (unsigned long long)SS.t);
+    else atomicAdd(&acc[k], v);
   }
   __syncthreads();
   if (threadIdx.x < kMetrics) out[threadIdx.x] = (long long)acc[threadIdx.x];

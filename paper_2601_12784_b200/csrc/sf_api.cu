@@ -36,6 +36,13 @@ struct sf_ctx {
   size_t stage_cap = 0;
   long long *d_dump = nullptr;
   size_t dump_cap = 0;
+  // live per-kernel timing (sf_profile): CUDA events recorded around every window kernel
+  int prof_on = 0;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<int> ev_kind;
+  size_t ev_used = 0;
+  double prof_ms[4] = {0, 0, 0, 0};
+  long long prof_n[4] = {0, 0, 0, 0};
 };
 
 namespace {
@@ -93,8 +100,9 @@ sf_status reduce_metrics_host(sf_ctx *c, long long *out) {
   return SF_OK;
 }
 
-sf_status check_errors(sf_ctx *c) {
-  // any poisoned scenario -> context poisoned
+// metric slot 29 of the reduction counts poisoned scenarios
+sf_status check_errors(sf_ctx *c, const long long *m) {
+  if (m[sf::M_ERR_SCEN] == 0) return SF_OK;
   std::vector<ScenState> ss(c->n_scen);
   if (!cuda_ok(c, cudaMemcpyAsync(ss.data(), c->D.ss, sizeof(ScenState) * c->n_scen, cudaMemcpyDeviceToHost, c->stream),
                "D2H states") ||
@@ -107,7 +115,19 @@ sf_status check_errors(sf_ctx *c) {
       return fail(c, SF_E_STATE, buf);
     }
   }
-  return SF_OK;
+  return fail(c, SF_E_STATE, "invariant violated");
+}
+
+void prof_mark(sf_ctx *c, int kind) {
+  if (!c->prof_on) return;
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev_pool.push_back(e);
+    c->ev_kind.push_back(0);
+  }
+  c->ev_kind[c->ev_used] = kind;
+  cudaEventRecord(c->ev_pool[c->ev_used++], c->stream);
 }
 
 }  // namespace
@@ -216,6 +236,7 @@ void sf_destroy(sf_ctx *c) {
   for (void *p : c->allocs) cudaFree(p);
   if (c->d_stage) cudaFree(c->d_stage);
   if (c->d_dump) cudaFree(c->d_dump);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   delete c;
 }
 
@@ -277,15 +298,21 @@ sf_status sf_step(sf_ctx *c, int32_t n_windows, sf_step_stats *out) {
   long long before[sf::kMetrics] = {0}, after[sf::kMetrics] = {0};
   if (out && (st = reduce_metrics_host(c, before)) != SF_OK) return st;
   for (int w = 0; w < n_windows; ++w) {
+    prof_mark(c, 0);
     sf_launch_begin_coord(c->P, c->D, c->n_scen, c->stream);
+    prof_mark(c, 0);
+    prof_mark(c, 1);
     sf_launch_advance(c->P, c->D, c->n_inst_total, c->stream);
+    prof_mark(c, 1);
+    prof_mark(c, 2);
     sf_launch_ledger(c->P, c->D, c->n_scen, c->stream);
+    prof_mark(c, 2);
     c->launches += 3;
   }
   if (!cuda_ok(c, cudaGetLastError(), "window launch")) return SF_E_CUDA;
   if (out) {
     if ((st = reduce_metrics_host(c, after)) != SF_OK) return st;
-    if ((st = check_errors(c)) != SF_OK) return st;
+    if ((st = check_errors(c, after)) != SF_OK) return st;
     out->windows = after[sf::M_WINDOWS] - before[sf::M_WINDOWS];
     out->ticks = after[sf::M_TICKS] - before[sf::M_TICKS];
     out->traj_iters = after[sf::M_TRAJ_ITERS] - before[sf::M_TRAJ_ITERS];
@@ -298,9 +325,7 @@ sf_status sf_step(sf_ctx *c, int32_t n_windows, sf_step_stats *out) {
     out->batches = after[sf::M_BATCHES] - before[sf::M_BATCHES];
     out->invalid_snapshots = after[sf::M_INVALID_SNAP] - before[sf::M_INVALID_SNAP];
     out->violations = after[sf::M_VIOLATIONS] - before[sf::M_VIOLATIONS];
-    ScenState s0;
-    if ((st = read_state(c, 0, &s0)) != SF_OK) return st;
-    out->sim_time_ps = s0.t;
+    out->sim_time_ps = after[sf::M_MAX_T];
   }
   return SF_OK;
 }
@@ -343,7 +368,9 @@ sf_status sf_collect_batch(sf_ctx *c, int32_t scenario, int32_t cap, int32_t *v_
     if (group_ids) group_ids[k] = h[2 + 2 * k];
     if (group_versions) group_versions[k] = h[3 + 2 * k];
   }
-  return check_errors(c);
+  long long m[sf::kMetrics];
+  if ((st = reduce_metrics_host(c, m)) != SF_OK) return st;
+  return check_errors(c, m);
 }
 
 sf_status sf_read_metrics(sf_ctx *c, int64_t *out, int32_t len) {
@@ -374,7 +401,8 @@ sf_status sf_read_scenario_metrics(sf_ctx *c, int32_t scenario, int64_t *out, in
   for (int k = 0; k < len; ++k) {
     long long v = k < sf::kMetrics ? (long long)s.m[k] : 0;
     if (k == sf::M_CMD_HASH) v = (long long)s.cmd_hash;
-    if (k == sf::M_SIM_TIME) v = s.t;
+    if (k == sf::M_SIM_TIME || k == sf::M_MAX_T) v = s.t;
+    if (k == sf::M_ERR_SCEN) v = s.err != 0;
     out[k] = v;
   }
   return SF_OK;
@@ -459,6 +487,33 @@ sf_status sf_dump_instances(sf_ctx *c, int32_t scenario, int64_t *out, int64_t c
 }
 
 int64_t sf_kernel_launches(const sf_ctx *c) { return c ? c->launches : 0; }
+
+sf_status sf_profile(sf_ctx *c, int32_t enable) {
+  sf_status st = check_ctx(c);
+  if (st != SF_OK) return st;
+  c->prof_on = enable ? 1 : 0;
+  return SF_OK;
+}
+
+sf_status sf_profile_read(sf_ctx *c, double *ms, int64_t *launches, int32_t len) {
+  sf_status st = check_ctx(c);
+  if (st != SF_OK) return st;
+  if (!cuda_ok(c, cudaStreamSynchronize(c->stream), "sync")) return SF_E_CUDA;
+  for (size_t k = 0; k + 1 < c->ev_used; k += 2) {
+    float e = 0.f;
+    if (!cuda_ok(c, cudaEventElapsedTime(&e, c->ev_pool[k], c->ev_pool[k + 1]), "event elapsed")) return SF_E_CUDA;
+    c->prof_ms[c->ev_kind[k]] += e;
+    c->prof_n[c->ev_kind[k]] += 1;
+  }
+  c->ev_used = 0;
+  for (int k = 0; k < len && k < 4; ++k) {
+    if (ms) ms[k] = c->prof_ms[k];
+    if (launches) launches[k] = c->prof_n[k];
+    c->prof_ms[k] = 0;
+    c->prof_n[k] = 0;
+  }
+  return SF_OK;
+}
 
 const char *sf_last_error(const sf_ctx *c) { return c ? c->err.c_str() : "null context"; }
 

@@ -26,7 +26,7 @@ STATUS = {0: "SF_OK", 1: "SF_NOT_READY", -1: "SF_E_INVALID", -2: "SF_E_VERSION",
 EXPORTS = ["sf_create", "sf_destroy", "sf_submit_prompts", "sf_submit_prompts_many", "sf_step",
            "sf_publish_params", "sf_collect_batch", "sf_read_metrics", "sf_read_metrics_device",
            "sf_read_scenario_metrics", "sf_dump_lifecycles", "sf_dump_batches", "sf_dump_commands",
-           "sf_dump_instances", "sf_kernel_launches", "sf_last_error"]
+           "sf_dump_instances", "sf_kernel_launches", "sf_last_error", "sf_profile", "sf_profile_read"]
 
 
 class SfConfig(C.Structure):
@@ -81,6 +81,8 @@ def load_library(path: str = LIB_PATH):
         "sf_dump_instances": (C.c_int, [P, I32, pI64, I64, pI64]),
         "sf_kernel_launches": (I64, [P]),
         "sf_last_error": (C.c_char_p, [P]),
+        "sf_profile": (C.c_int, [P, I32]),
+        "sf_profile_read": (C.c_int, [P, C.POINTER(C.c_double), pI64, I32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -242,6 +244,16 @@ class StaleFlow:
 
     def instances(self, scen: int) -> np.ndarray:
         return self._dump(self.L.sf_dump_instances, scen, 7, np.int64, C.c_int64)
+
+    def profile(self, enable: bool = True):
+        self._check(self.L.sf_profile(self.h, int(enable)), "sf_profile")
+
+    def profile_read(self):
+        """(ms[4], launches[4]) per window kernel: coordinate, advance, ledger, -."""
+        ms = np.zeros(4, np.float64)
+        n = np.zeros(4, np.int64)
+        self._check(self.L.sf_profile_read(self.h, _p(ms, C.c_double), _p(n, C.c_int64), 4), "sf_profile_read")
+        return ms, n
 
     @property
     def kernel_launches(self) -> int:
