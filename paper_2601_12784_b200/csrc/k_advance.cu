@@ -2,65 +2,265 @@
 // (DESIGN.md §3.1 W6-W7, boundary procedure §3.2 B1-B8).
 //
 // One warp per instance; instances are independent inside a window (W7), which is the data
-// parallelism of the step.  Per decode step the warp streams the instance's run list
-// (`run_rem`, int32 remaining tokens; `run_id` only for compaction) with coalesced lane-
-// contiguous loads, decrements every counter (one token per running trajectory),
-// detects completions with __ballot_sync, compacts the survivors in place (stable, so the run
-// list stays in admission order for LIFO preemption), and reduces the released KV with warp
-// shuffles.  Everything per-instance (KV, counts, next step time) stays in registers across
-// all steps of the window.
+// parallelism of the step.  Fast path (every instance whose run+wait+arrivals fit 32*kR): the
+// instance's run list is staged ONCE per window from HBM into registers -- lane l holds run
+// slots l, l+32, ... with a warp-uniform live bitmask per register row -- and every decode
+// step of the window decrements the remaining-length counters in registers (one token per
+// running trajectory), detects completions with __ballot_sync, and reduces the
+// released KV with warp shuffles only when something completed.  Slot order = admission order,
+// so completions leave holes (compacted lazily through shared memory) and LIFO preemption
+// takes the highest live slot.  The list is written back compacted at the window end.
+// Fallback path: the same procedure streaming the run list through global memory.
 #include "sf_internal.cuh"
 
 namespace sf {
 
 constexpr long long kInf = 0x7fffffffffffffffLL;
+constexpr int kR = 4;                      // register rows -> 128 run slots per instance
+constexpr int kWarpsPerBlock = 8;
 
-__global__ void __launch_bounds__(256) k_advance(GParams P, Dev D, int n_inst_total) {
-  const int gi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (gi >= n_inst_total) return;
+struct InstState {
+  int st, pullv, pullpend, intkind, intk, cc, v, run_n, whead, wn, arr_n, arr_head;
+  long long nb, until, kv, prefill, t_cmd;
+  long long ticks, iters, tokens, comps, preempts;
+};
+
+__device__ __forceinline__ void emit_completion(const GParams &P, const Dev &D, const ScenConst &C, ScenState &SS,
+                                                int id, long long b, long long &release) {
+  const long long j = C.traj_off + id;
+  const int Tj = D.T[j];
+  release += (long long)P.k5 * (long long)(D.prompt[C.grp_off + id / P.G] + Tj);
+  D.gen[j] = Tj;
+  D.loc[j] = L_DONE;
+  D.t_complete[j] = b;                      // reward due at b + R
+  const int e = atomicAdd(&SS.ev_n, 1);
+  D.ev_id[C.ev_off + e] = id;
+}
+
+// ------------------------------------------------------------------ register-resident path
+__device__ void advance_reg(const GParams &P, const Dev &D, const ScenConst &C, ScenState &SS, InstState &x,
+                            long long lb, long long t_end, int2 *stage) {
   const unsigned lane = lane_id();
-  const int s = D.inst_scen[gi];
-  const ScenConst C = D.sc[s];
-  ScenState &SS = D.ss[s];
-  if (SS.err) return;
-  const int i = gi - C.inst_off;
-  const long long t = SS.t, t_end = t + P.delta;
-  const long long lb = C.list_off + (long long)i * C.cap;
   const int cap = C.cap;
-  const int G = P.G;
   const long long k5 = P.k5;
-
-  int st = D.ist[gi];
-  long long nb = D.inb[gi], until = D.iuntil[gi];
-  int pullv = D.ipullv[gi], pullpend = D.ipullpend[gi];
-  int intkind = D.iintkind[gi], intk = D.iintk[gi];
-  long long kv = D.ikv[gi], prefill = D.iprefill[gi];
-  int cc = D.ic[gi], v = D.iv[gi];
-  int run_n = D.irun_n[gi], whead = D.iwhead[gi], wn = D.iwn[gi];
-  const int arr_n = D.iarr_n[gi];
-  int arr_head = 0;
-  long long ticks = 0, iters = 0, tokens = 0, comps = 0, preempts = 0;
-  // W6: commands to an idle instance apply at a boundary at t
-  long long t_cmd = (st == I_IDLE && (pullpend || intkind != INT_NONE)) ? t : kInf;
+  int rem[kR], rid[kR];
+  unsigned live[kR];
+#pragma unroll
+  for (int q = 0; q < kR; ++q) {
+    const int s = q * 32 + (int)lane;
+    rem[q] = 0; rid[q] = 0;
+    if (s < x.run_n) { rem[q] = D.run_rem[lb + s]; rid[q] = D.run_id[lb + s]; }
+    live[q] = __ballot_sync(0xffffffffu, s < x.run_n);
+  }
+  int nlive = x.run_n, tail = x.run_n;
+  long long next_arr = x.arr_head < x.arr_n ? D.arr_t[lb + x.arr_head] : kInf;
+  bool head_ok = false;
+  int head_id = 0, head_gen = 0, head_T = 0;
+  long long head_ctx = 0;
 
   for (;;) {
     long long b;
-    if (st == I_TICK) b = nb;
-    else if (st == I_PULL) b = until;
-    else b = min(t_cmd, arr_head < arr_n ? D.arr_t[lb + arr_head] : kInf);
+    if (x.st == I_TICK) b = x.nb;
+    else if (x.st == I_PULL) b = x.until;
+    else b = min(x.t_cmd, next_arr);
     if (b == kInf || b > t_end) break;
-    t_cmd = kInf;
-    const bool tick_end = (st == I_TICK);
-    const bool pull_done = (st == I_PULL);
+    x.t_cmd = kInf;
+    const bool tick_end = (x.st == I_TICK);
+    const bool pull_done = (x.st == I_PULL);
     // B1: pending interrupts leave without this step's token; KV released (A17, A18)
-    if (!pull_done && intkind != INT_NONE) {
-      if (intkind == INT_ALL) { run_n = 0; wn = 0; kv = 0; }
-      else wn -= intk;                                  // wait tail (A7)
-      intkind = INT_NONE;
+    if (!pull_done && x.intkind != INT_NONE) {
+      if (x.intkind == INT_ALL) {
+#pragma unroll
+        for (int q = 0; q < kR; ++q) live[q] = 0u;
+        nlive = 0; tail = 0; x.wn = 0; x.kv = 0;
+      } else {
+        x.wn -= x.intk;                                  // wait tail (A7)
+      }
+      if (x.wn == 0) head_ok = false;
+      x.intkind = INT_NONE;
     }
     if (tick_end) {
-      // B2 + B3: credit one token to every running trajectory; completions leave in order
-      const int n0 = run_n;
+      // B2 + B3 in registers
+      const int n0 = nlive;
+      int ncomp = 0;
+      long long release = 0;
+#pragma unroll
+      for (int q = 0; q < kR; ++q) {
+        if (q * 32 < tail) {
+          const bool lv = (live[q] >> lane) & 1u;
+          if (lv) rem[q] -= 1;
+          const unsigned d = __ballot_sync(0xffffffffu, lv && rem[q] == 0);
+          if (d) {
+            if ((d >> lane) & 1u) emit_completion(P, D, C, SS, rid[q], b, release);
+            live[q] &= ~d;
+            ncomp += __popc(d);
+          }
+        }
+      }
+      if (ncomp) {
+        release = warp_sum(release);
+        nlive -= ncomp;
+        x.cc += ncomp;
+        x.comps += ncomp;
+        // shrink the tail to the highest live slot
+        int t = 0;
+#pragma unroll
+        for (int q = 0; q < kR; ++q)
+          if (live[q]) t = q * 32 + 32 - __clz(live[q]);
+        tail = t;
+      }
+      x.kv += k5 * n0 - release;
+      x.tokens += n0;
+      x.st = I_IDLE;
+    }
+    if (pull_done) { x.v = x.pullv; x.cc = 0; x.st = I_IDLE; }
+    // B4: preemption while KV exceeds M: newest admitted (highest live slot) -> wait front (A21)
+    while (x.kv > P.M && nlive > 0) {
+      int hq = 0;
+#pragma unroll
+      for (int q = 0; q < kR; ++q)
+        if (live[q]) hq = q;
+      unsigned hm = 0;
+      int r_ = 0, i_ = 0;
+#pragma unroll
+      for (int q = 0; q < kR; ++q)
+        if (q == hq) { hm = live[q]; r_ = rem[q]; i_ = rid[q]; }
+      const int hl = 31 - __clz(hm);
+      const int r = __shfl_sync(0xffffffffu, r_, hl);
+      const int id = __shfl_sync(0xffffffffu, i_, hl);
+      const long long j = C.traj_off + id;
+      const int Tj = D.T[j];
+      const int g_ = Tj - r;
+      x.kv -= k5 * (long long)(D.prompt[C.grp_off + id / P.G] + g_);
+      x.whead = x.whead == 0 ? cap - 1 : x.whead - 1;
+      if (lane == 0) {
+        D.gen[j] = g_;
+        D.loc[j] = L_WAIT;
+        D.n_preempt[j] += 1;
+        D.wait_id[lb + x.whead] = id;
+      }
+#pragma unroll
+      for (int q = 0; q < kR; ++q)
+        if (q == hq) live[q] &= ~(1u << hl);
+      --nlive;
+      tail = hq * 32 + hl;
+      ++x.wn;
+      ++x.preempts;
+      head_ok = true; head_id = id; head_gen = g_; head_T = Tj;
+      head_ctx = D.prompt[C.grp_off + id / P.G] + g_;
+    }
+    // B5: a pending Pull blocks generation for q (P:909, 922)
+    if (x.pullpend) {
+      x.pullpend = 0;
+      x.st = I_PULL;
+      x.until = b + P.q;
+      continue;
+    }
+    // B6: arrivals with t_arr <= b join the wait tail in (t_arr, id) order (P:585)
+    while (next_arr <= b) {
+      const int id = D.arr_id[lb + x.arr_head];
+      int pos = x.whead + x.wn;
+      if (pos >= cap) pos -= cap;
+      if (lane == 0) { D.wait_id[lb + pos] = id; D.loc[C.traj_off + id] = L_WAIT; }
+      ++x.wn;
+      ++x.arr_head;
+      next_arr = x.arr_head < x.arr_n ? D.arr_t[lb + x.arr_head] : kInf;
+    }
+    __syncwarp();
+    // B7: FIFO admission while the head fits the KV budget (P:650)
+    while (x.wn > 0) {
+      if (!head_ok) {
+        head_id = D.wait_id[lb + x.whead];
+        const long long j = C.traj_off + head_id;
+        head_gen = D.gen[j];
+        head_T = D.T[j];
+        head_ctx = D.prompt[C.grp_off + head_id / P.G] + head_gen;
+        head_ok = true;
+      }
+      if (x.kv + k5 * head_ctx > P.M) break;
+      if (tail == 32 * kR) {
+        // stable compaction of the live slots through shared memory
+#pragma unroll
+        for (int q = 0; q < kR; ++q) {
+          int before = 0;
+#pragma unroll
+          for (int qq = 0; qq < kR; ++qq)
+            if (qq < q) before += __popc(live[qq]);
+          if ((live[q] >> lane) & 1u) stage[before + __popc(live[q] & lanemask_lt())] = make_int2(rem[q], rid[q]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < kR; ++q) {
+          const int s = q * 32 + (int)lane;
+          if (s < nlive) { const int2 e = stage[s]; rem[q] = e.x; rid[q] = e.y; }
+          live[q] = __ballot_sync(0xffffffffu, s < nlive);
+        }
+        __syncwarp();
+        tail = nlive;
+      }
+      const int s = tail++;
+      const int sq = s >> 5, sl = s & 31;
+#pragma unroll
+      for (int q = 0; q < kR; ++q)
+        if (q == sq) {
+          if ((int)lane == sl) { rem[q] = head_T - head_gen; rid[q] = head_id; }
+          live[q] |= 1u << sl;
+        }
+      if (lane == 0) D.loc[C.traj_off + head_id] = L_RUN;
+      x.kv += k5 * head_ctx;
+      x.prefill += head_ctx;
+      ++nlive;
+      x.whead = x.whead + 1 == cap ? 0 : x.whead + 1;
+      --x.wn;
+      head_ok = false;
+    }
+    // B8: next decode step, Eq 7 + prefill stall (P:1046-1051, A20)
+    if (nlive > 0) {
+      x.nb = b + tick_latency(P, x.kv, nlive, x.prefill);
+      x.prefill = 0;
+      x.st = I_TICK;
+      x.iters += nlive;
+      ++x.ticks;
+    } else {
+      x.st = I_IDLE;
+    }
+  }
+  // write the run list back compacted, in admission order
+  int before = 0;
+#pragma unroll
+  for (int q = 0; q < kR; ++q) {
+    if ((live[q] >> lane) & 1u) {
+      const int pos = before + __popc(live[q] & lanemask_lt());
+      D.run_rem[lb + pos] = rem[q];
+      D.run_id[lb + pos] = rid[q];
+    }
+    before += __popc(live[q]);
+  }
+  x.run_n = nlive;
+}
+
+// ------------------------------------------------------------------ global-memory path
+__device__ void advance_global(const GParams &P, const Dev &D, const ScenConst &C, ScenState &SS, InstState &x,
+                               long long lb, long long t_end) {
+  const unsigned lane = lane_id();
+  const int cap = C.cap;
+  const long long k5 = P.k5;
+  for (;;) {
+    long long b;
+    if (x.st == I_TICK) b = x.nb;
+    else if (x.st == I_PULL) b = x.until;
+    else b = min(x.t_cmd, x.arr_head < x.arr_n ? D.arr_t[lb + x.arr_head] : kInf);
+    if (b == kInf || b > t_end) break;
+    x.t_cmd = kInf;
+    const bool tick_end = (x.st == I_TICK);
+    const bool pull_done = (x.st == I_PULL);
+    if (!pull_done && x.intkind != INT_NONE) {
+      if (x.intkind == INT_ALL) { x.run_n = 0; x.wn = 0; x.kv = 0; }
+      else x.wn -= x.intk;
+      x.intkind = INT_NONE;
+    }
+    if (tick_end) {
+      const int n0 = x.run_n;
       int out = 0, ncomp = 0;
       long long release = 0;
       for (int base = 0; base < n0; base += 32) {
@@ -75,125 +275,139 @@ __global__ void __launch_bounds__(256) k_advance(GParams P, Dev D, int n_inst_to
         const int pos = out + __popc(mk & lanemask_lt());
         __syncwarp();
         if (keep) { D.run_rem[lb + pos] = rem; D.run_id[lb + pos] = id; }
-        if (done) {
-          const long long j = C.traj_off + id;
-          const int Tj = D.T[j];
-          release += k5 * (long long)(D.prompt[C.grp_off + id / G] + Tj);
-          D.gen[j] = Tj;
-          D.loc[j] = L_DONE;
-          D.t_complete[j] = b;                          // reward due at b + R
-          const int e = atomicAdd(&SS.ev_n, 1);
-          D.ev_id[C.ev_off + e] = id;
-        }
+        if (done) emit_completion(P, D, C, SS, id, b, release);
         out += __popc(mk);
         ncomp += __popc(md);
       }
-      release = warp_sum(release);
-      kv += k5 * n0 - release;
-      tokens += n0;
-      run_n = out;
-      cc += ncomp;
-      comps += ncomp;
-      st = I_IDLE;
+      if (ncomp) release = warp_sum(release);
+      x.kv += k5 * n0 - release;
+      x.tokens += n0;
+      x.run_n = out;
+      x.cc += ncomp;
+      x.comps += ncomp;
+      x.st = I_IDLE;
       __syncwarp();
     }
-    if (pull_done) { v = pullv; cc = 0; st = I_IDLE; }
-    // B4: preemption while KV exceeds M: newest admitted -> wait front (A21)
-    while (kv > P.M && run_n > 0) {
-      const int k = run_n - 1;
+    if (pull_done) { x.v = x.pullv; x.cc = 0; x.st = I_IDLE; }
+    while (x.kv > P.M && x.run_n > 0) {
+      const int k = x.run_n - 1;
       const int id = D.run_id[lb + k];
       const long long j = C.traj_off + id;
       const int g_ = D.T[j] - D.run_rem[lb + k];
-      kv -= k5 * (long long)(D.prompt[C.grp_off + id / G] + g_);
-      whead = whead == 0 ? cap - 1 : whead - 1;
+      x.kv -= k5 * (long long)(D.prompt[C.grp_off + id / P.G] + g_);
+      x.whead = x.whead == 0 ? cap - 1 : x.whead - 1;
       if (lane == 0) {
         D.gen[j] = g_;
         D.loc[j] = L_WAIT;
         D.n_preempt[j] += 1;
-        D.wait_id[lb + whead] = id;
+        D.wait_id[lb + x.whead] = id;
       }
-      ++wn;
-      --run_n;
-      ++preempts;
+      ++x.wn;
+      --x.run_n;
+      ++x.preempts;
     }
-    // B5: a pending Pull blocks generation for q (P:909, 922)
-    if (pullpend) {
-      pullpend = 0;
-      st = I_PULL;
-      until = b + P.q;
+    if (x.pullpend) {
+      x.pullpend = 0;
+      x.st = I_PULL;
+      x.until = b + P.q;
       __syncwarp();
       continue;
     }
-    // B6: arrivals with t_arr <= b join the wait tail in (t_arr, id) order (P:585)
-    while (arr_head < arr_n && D.arr_t[lb + arr_head] <= b) {
-      const int id = D.arr_id[lb + arr_head];
-      int pos = whead + wn;
+    while (x.arr_head < x.arr_n && D.arr_t[lb + x.arr_head] <= b) {
+      const int id = D.arr_id[lb + x.arr_head];
+      int pos = x.whead + x.wn;
       if (pos >= cap) pos -= cap;
       if (lane == 0) { D.wait_id[lb + pos] = id; D.loc[C.traj_off + id] = L_WAIT; }
-      ++wn;
-      ++arr_head;
+      ++x.wn;
+      ++x.arr_head;
     }
     __syncwarp();
-    // B7: FIFO admission while the head fits the KV budget (P:650)
-    while (wn > 0) {
-      const int id = D.wait_id[lb + whead];
+    while (x.wn > 0) {
+      const int id = D.wait_id[lb + x.whead];
       const long long j = C.traj_off + id;
       const int gj = D.gen[j];
-      const long long ctx = D.prompt[C.grp_off + id / G] + gj;
-      if (kv + k5 * ctx > P.M) break;
+      const long long ctx = D.prompt[C.grp_off + id / P.G] + gj;
+      if (x.kv + k5 * ctx > P.M) break;
       if (lane == 0) {
-        D.run_id[lb + run_n] = id;
-        D.run_rem[lb + run_n] = D.T[j] - gj;
+        D.run_id[lb + x.run_n] = id;
+        D.run_rem[lb + x.run_n] = D.T[j] - gj;
         D.loc[j] = L_RUN;
       }
-      kv += k5 * ctx;
-      prefill += ctx;
-      ++run_n;
-      whead = whead + 1 == cap ? 0 : whead + 1;
-      --wn;
+      x.kv += k5 * ctx;
+      x.prefill += ctx;
+      ++x.run_n;
+      x.whead = x.whead + 1 == cap ? 0 : x.whead + 1;
+      --x.wn;
     }
     __syncwarp();
-    // B8: next decode step, Eq 7 + prefill stall (P:1046-1051, A20)
-    if (run_n > 0) {
-      nb = b + tick_latency(P, kv, run_n, prefill);
-      prefill = 0;
-      st = I_TICK;
-      iters += run_n;
-      ++ticks;
+    if (x.run_n > 0) {
+      x.nb = b + tick_latency(P, x.kv, x.run_n, x.prefill);
+      x.prefill = 0;
+      x.st = I_TICK;
+      x.iters += x.run_n;
+      ++x.ticks;
     } else {
-      st = I_IDLE;
+      x.st = I_IDLE;
     }
   }
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerBlock) k_advance(GParams P, Dev D, int n_inst_total) {
+  __shared__ int2 stage_all[kWarpsPerBlock][32 * kR];
+  const int gi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (gi >= n_inst_total) return;
+  const unsigned lane = lane_id();
+  const int s = D.inst_scen[gi];
+  const ScenConst C = D.sc[s];
+  ScenState &SS = D.ss[s];
+  if (SS.err) return;
+  const int i = gi - C.inst_off;
+  const long long t = SS.t, t_end = t + P.delta;
+  const long long lb = C.list_off + (long long)i * C.cap;
+
+  InstState x;
+  x.st = D.ist[gi]; x.nb = D.inb[gi]; x.until = D.iuntil[gi];
+  x.pullv = D.ipullv[gi]; x.pullpend = D.ipullpend[gi];
+  x.intkind = D.iintkind[gi]; x.intk = D.iintk[gi];
+  x.kv = D.ikv[gi]; x.prefill = D.iprefill[gi]; x.cc = D.ic[gi]; x.v = D.iv[gi];
+  x.run_n = D.irun_n[gi]; x.whead = D.iwhead[gi]; x.wn = D.iwn[gi];
+  x.arr_n = D.iarr_n[gi]; x.arr_head = 0;
+  x.ticks = x.iters = x.tokens = x.comps = x.preempts = 0;
+  // W6: commands to an idle instance apply at a boundary at t
+  x.t_cmd = (x.st == I_IDLE && (x.pullpend || x.intkind != INT_NONE)) ? t : kInf;
+
+  if (x.run_n + x.wn + x.arr_n <= 32 * kR) advance_reg(P, D, C, SS, x, lb, t_end, stage_all[threadIdx.x >> 5]);
+  else advance_global(P, D, C, SS, x, lb, t_end);
+
   // keep undelivered arrivals (held while pulling / later than the window) at the list front
-  const int remain = arr_n - arr_head;
-  if (arr_head > 0 && remain > 0) {
+  const int remain = x.arr_n - x.arr_head;
+  if (x.arr_head > 0 && remain > 0) {
     for (int k0 = 0; k0 < remain; k0 += 32) {
       const int k = k0 + (int)lane;
       long long ta = 0;
       int ia = 0;
-      if (k < remain) { ta = D.arr_t[lb + arr_head + k]; ia = D.arr_id[lb + arr_head + k]; }
+      if (k < remain) { ta = D.arr_t[lb + x.arr_head + k]; ia = D.arr_id[lb + x.arr_head + k]; }
       __syncwarp();
       if (k < remain) { D.arr_t[lb + k] = ta; D.arr_id[lb + k] = ia; }
       __syncwarp();
     }
   }
   if (lane == 0) {
-    D.ist[gi] = st; D.inb[gi] = nb; D.iuntil[gi] = until;
-    D.ipullpend[gi] = pullpend; D.iintkind[gi] = intkind;
-    D.ikv[gi] = kv; D.iprefill[gi] = prefill; D.ic[gi] = cc; D.iv[gi] = v;
-    D.irun_n[gi] = run_n; D.iwhead[gi] = whead; D.iwn[gi] = wn; D.iarr_n[gi] = remain;
-    metric_add(SS, M_TICKS, ticks);
-    metric_add(SS, M_TRAJ_ITERS, iters);
-    metric_add(SS, M_TOKENS, tokens);
-    metric_add(SS, M_COMPLETIONS, comps);
-    metric_add(SS, M_PREEMPTIONS, preempts);
+    D.ist[gi] = x.st; D.inb[gi] = x.nb; D.iuntil[gi] = x.until;
+    D.ipullpend[gi] = x.pullpend; D.iintkind[gi] = x.intkind;
+    D.ikv[gi] = x.kv; D.iprefill[gi] = x.prefill; D.ic[gi] = x.cc; D.iv[gi] = x.v;
+    D.irun_n[gi] = x.run_n; D.iwhead[gi] = x.whead; D.iwn[gi] = x.wn; D.iarr_n[gi] = remain;
+    metric_add(SS, M_TICKS, x.ticks);
+    metric_add(SS, M_TRAJ_ITERS, x.iters);
+    metric_add(SS, M_TOKENS, x.tokens);
+    metric_add(SS, M_COMPLETIONS, x.comps);
+    metric_add(SS, M_PREEMPTIONS, x.preempts);
   }
 }
 
 }  // namespace sf
 
 void sf_launch_advance(const sf::GParams &P, const sf::Dev &D, int n_inst_total, cudaStream_t st) {
-  const int warps_per_block = 8;
-  const int blocks = (n_inst_total + warps_per_block - 1) / warps_per_block;
-  sf::k_advance<<<blocks, 32 * warps_per_block, 0, st>>>(P, D, n_inst_total);
+  const int blocks = (n_inst_total + sf::kWarpsPerBlock - 1) / sf::kWarpsPerBlock;
+  sf::k_advance<<<blocks, 32 * sf::kWarpsPerBlock, 0, st>>>(P, D, n_inst_total);
 }

@@ -23,6 +23,7 @@ struct sf_ctx {
   std::vector<ScenConst> hsc;
   std::vector<int> hn_pool;
   int n_inst_total = 0;
+  int max_inst = 1;
   int n_scen = 0;
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -166,7 +167,7 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
     S.I = cfg->scenario_instances ? cfg->scenario_instances[s] : instances;
     S.eta = cfg->scenario_eta ? cfg->scenario_eta[s] : eta;
     S.strategy = (int)(cfg->scenario_strategy ? cfg->scenario_strategy[s] : cfg->strategy);
-    if (S.I < 1 || S.I > sf::kMaxInst || S.eta < 0 || S.eta > sf::kMaxEta) {
+    if (S.I < 1 || S.I > sf::kMaxInst || S.eta < 0 || S.eta > sf::kMaxEta || pool_traj >= (1LL << 27)) {
       delete c;
       return SF_E_INVALID;
     }
@@ -174,6 +175,7 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
     S.inst_off = (int)inst; S.grp_off = s * P.pool_cap; S.led_off = (int)led; S.ring_off = (int)ring;
     S.traj_off = (long long)s * pool_traj; S.list_off = list; S.bits_off = bits; S.mlq_off = mlq;
     S.ev_off = ev; S.batch_off = batch; S.cmd_off = cmd;
+    c->max_inst = std::max(c->max_inst, S.I);
     inst += S.I; led += (long long)(S.eta + 1) * B; ring += S.eta + 1; list += (long long)S.I * S.cap;
     bits += bwords; mlq += 2LL * S.cap; ev += S.cap; batch += batch_rec; cmd += 4LL * P.cmdlog_cap;
   }
@@ -299,7 +301,7 @@ sf_status sf_step(sf_ctx *c, int32_t n_windows, sf_step_stats *out) {
   if (out && (st = reduce_metrics_host(c, before)) != SF_OK) return st;
   for (int w = 0; w < n_windows; ++w) {
     prof_mark(c, 0);
-    sf_launch_begin_coord(c->P, c->D, c->n_scen, c->stream);
+    sf_launch_begin_coord(c->P, c->D, c->n_scen, c->max_inst, c->stream);
     prof_mark(c, 0);
     prof_mark(c, 1);
     sf_launch_advance(c->P, c->D, c->n_inst_total, c->stream);
