@@ -50,10 +50,11 @@ typedef struct {
   const int32_t *scenario_eta;        /* [n_scenarios] or NULL (= eta argument)                 */
   const int32_t *scenario_instances;  /* [n_scenarios] or NULL (= instances argument), <= 128   */
   const uint32_t *scenario_strategy;  /* [n_scenarios] or NULL (= strategy)                     */
-  int64_t k1_ps_per_tok, k2_ps, k3_ps, k4_ps;   /* Eq 7 coefficients (Table 6) in ps  */
+  int64_t k1_ps_per_tok, k2_ps, k3_ps, k4_ps;   /* Eq 7 coefficients (Table 6) in ps; */
+                                      /*   k1, k3 < 2^31 (SF_E_INVALID otherwise)               */
   int32_t k5_tok;                     /* KV tokens per token, >= 1                       */
-  int64_t kprefill_ps_per_tok;        /* prefill stall per admitted token (A20)        */
-  int64_t kv_budget_tok;              /* M                                               */
+  int64_t kprefill_ps_per_tok;        /* prefill stall per admitted token (A20), < 2^31 */
+  int64_t kv_budget_tok;              /* M, < 2^30                                       */
   double mu, phi_throughput;          /* waterfall threshold, migration gap              */
   int32_t phi_wait;                   /* migration wait threshold                        */
   int64_t snap_period_ps;             /* Delta: one sf_step window                               */

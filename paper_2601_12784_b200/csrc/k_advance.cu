@@ -38,6 +38,12 @@ __device__ __forceinline__ void emit_completion(const GParams &P, const Dev &D, 
 }
 
 // ------------------------------------------------------------------ register-resident path
+// Dead / empty slots hold a sentinel remaining length (kDead) so a decode step is a plain
+// decrement + ballot per register row with no live-mask test; a window has far fewer than kDead
+// steps.  `blocked` records that the wait-queue head did not fit the KV budget and that no KV
+// has been released since (KV only grows on a quiet step), so quiet steps skip B7.
+constexpr int kDead = 1 << 30;
+
 __device__ void advance_reg(const GParams &P, const Dev &D, const ScenConst &C, ScenState &SS, InstState &x,
                             long long lb, long long t_end, int2 *stage) {
   const unsigned lane = lane_id();
@@ -48,22 +54,24 @@ __device__ void advance_reg(const GParams &P, const Dev &D, const ScenConst &C, 
 #pragma unroll
   for (int q = 0; q < kR; ++q) {
     const int s = q * 32 + (int)lane;
-    rem[q] = 0; rid[q] = 0;
+    rem[q] = kDead; rid[q] = 0;
     if (s < x.run_n) { rem[q] = D.run_rem[lb + s]; rid[q] = D.run_id[lb + s]; }
     live[q] = __ballot_sync(0xffffffffu, s < x.run_n);
   }
   int nlive = x.run_n, tail = x.run_n;
   long long next_arr = x.arr_head < x.arr_n ? D.arr_t[lb + x.arr_head] : kInf;
-  bool head_ok = false;
+  bool head_ok = false, blocked = false;
   int head_id = 0, head_gen = 0, head_T = 0;
   long long head_ctx = 0;
+  int cn_n = -1;
+  long long cn = 0;                                   // max(k2, k3 n) + k4 for n = cn_n
 
   for (;;) {
     long long b;
     if (x.st == I_TICK) b = x.nb;
     else if (x.st == I_PULL) b = x.until;
     else b = min(x.t_cmd, next_arr);
-    if (b == kInf || b > t_end) break;
+    if (b > t_end) break;                             // kInf > t_end
     x.t_cmd = kInf;
     const bool tick_end = (x.st == I_TICK);
     const bool pull_done = (x.st == I_PULL);
@@ -71,83 +79,92 @@ __device__ void advance_reg(const GParams &P, const Dev &D, const ScenConst &C, 
     if (!pull_done && x.intkind != INT_NONE) {
       if (x.intkind == INT_ALL) {
 #pragma unroll
-        for (int q = 0; q < kR; ++q) live[q] = 0u;
+        for (int q = 0; q < kR; ++q) { live[q] = 0u; rem[q] = kDead; }
         nlive = 0; tail = 0; x.wn = 0; x.kv = 0;
       } else {
         x.wn -= x.intk;                                  // wait tail (A7)
       }
       if (x.wn == 0) head_ok = false;
+      blocked = false;
       x.intkind = INT_NONE;
     }
     if (tick_end) {
-      // B2 + B3 in registers
+      // B2 + B3 in registers: one token per running trajectory, ballot the completions
       const int n0 = nlive;
-      int ncomp = 0;
-      long long release = 0;
+      unsigned d[kR], dany = 0;
 #pragma unroll
       for (int q = 0; q < kR; ++q) {
-        if (q * 32 < tail) {
-          const bool lv = (live[q] >> lane) & 1u;
-          if (lv) rem[q] -= 1;
-          const unsigned d = __ballot_sync(0xffffffffu, lv && rem[q] == 0);
-          if (d) {
-            if ((d >> lane) & 1u) emit_completion(P, D, C, SS, rid[q], b, release);
-            live[q] &= ~d;
-            ncomp += __popc(d);
-          }
-        }
+        rem[q] -= 1;
+        d[q] = __ballot_sync(0xffffffffu, rem[q] == 0);
+        dany |= d[q];
       }
-      if (ncomp) {
+      x.kv += k5 * n0;
+      x.tokens += n0;
+      if (dany) {
+        long long release = 0;
+        int ncomp = 0;
+#pragma unroll
+        for (int q = 0; q < kR; ++q) {
+          if ((d[q] >> lane) & 1u) { emit_completion(P, D, C, SS, rid[q], b, release); rem[q] = kDead; }
+          live[q] &= ~d[q];
+          ncomp += __popc(d[q]);
+        }
         release = warp_sum(release);
+        x.kv -= release;
         nlive -= ncomp;
         x.cc += ncomp;
         x.comps += ncomp;
-        // shrink the tail to the highest live slot
         int t = 0;
 #pragma unroll
         for (int q = 0; q < kR; ++q)
           if (live[q]) t = q * 32 + 32 - __clz(live[q]);
         tail = t;
+        blocked = false;
       }
-      x.kv += k5 * n0 - release;
-      x.tokens += n0;
       x.st = I_IDLE;
+    } else if (pull_done) {
+      x.v = x.pullv; x.cc = 0; x.st = I_IDLE;
     }
-    if (pull_done) { x.v = x.pullv; x.cc = 0; x.st = I_IDLE; }
     // B4: preemption while KV exceeds M: newest admitted (highest live slot) -> wait front (A21)
-    while (x.kv > P.M && nlive > 0) {
-      int hq = 0;
+    if (x.kv > P.M) {
+      while (x.kv > P.M && nlive > 0) {
+        int hq = 0;
 #pragma unroll
-      for (int q = 0; q < kR; ++q)
-        if (live[q]) hq = q;
-      unsigned hm = 0;
-      int r_ = 0, i_ = 0;
+        for (int q = 0; q < kR; ++q)
+          if (live[q]) hq = q;
+        unsigned hm = 0;
+        int r_ = 0, i_ = 0;
 #pragma unroll
-      for (int q = 0; q < kR; ++q)
-        if (q == hq) { hm = live[q]; r_ = rem[q]; i_ = rid[q]; }
-      const int hl = 31 - __clz(hm);
-      const int r = __shfl_sync(0xffffffffu, r_, hl);
-      const int id = __shfl_sync(0xffffffffu, i_, hl);
-      const long long j = C.traj_off + id;
-      const int Tj = D.T[j];
-      const int g_ = Tj - r;
-      x.kv -= k5 * (long long)(D.prompt[C.grp_off + id / P.G] + g_);
-      x.whead = x.whead == 0 ? cap - 1 : x.whead - 1;
-      if (lane == 0) {
-        D.gen[j] = g_;
-        D.loc[j] = L_WAIT;
-        D.n_preempt[j] += 1;
-        D.wait_id[lb + x.whead] = id;
+        for (int q = 0; q < kR; ++q)
+          if (q == hq) { hm = live[q]; r_ = rem[q]; i_ = rid[q]; }
+        const int hl = 31 - __clz(hm);
+        const int r = __shfl_sync(0xffffffffu, r_, hl);
+        const int id = __shfl_sync(0xffffffffu, i_, hl);
+        const long long j = C.traj_off + id;
+        const int Tj = D.T[j];
+        const int g_ = Tj - r;
+        const long long ctx = D.prompt[C.grp_off + id / P.G] + g_;
+        x.kv -= k5 * ctx;
+        x.whead = x.whead == 0 ? cap - 1 : x.whead - 1;
+        if (lane == 0) {
+          D.gen[j] = g_;
+          D.loc[j] = L_WAIT;
+          D.n_preempt[j] += 1;
+          D.wait_id[lb + x.whead] = id;
+        }
+#pragma unroll
+        for (int q = 0; q < kR; ++q)
+          if (q == hq) {
+            live[q] &= ~(1u << hl);
+            if ((int)lane == hl) rem[q] = kDead;
+          }
+        --nlive;
+        tail = hq * 32 + hl;
+        ++x.wn;
+        ++x.preempts;
+        head_ok = true; head_id = id; head_gen = g_; head_T = Tj; head_ctx = ctx;
       }
-#pragma unroll
-      for (int q = 0; q < kR; ++q)
-        if (q == hq) live[q] &= ~(1u << hl);
-      --nlive;
-      tail = hq * 32 + hl;
-      ++x.wn;
-      ++x.preempts;
-      head_ok = true; head_id = id; head_gen = g_; head_T = Tj;
-      head_ctx = D.prompt[C.grp_off + id / P.G] + g_;
+      blocked = true;                                 // the last victim (the head) cannot re-fit now
     }
     // B5: a pending Pull blocks generation for q
     if (x.pullpend) {
@@ -157,72 +174,102 @@ __device__ void advance_reg(const GParams &P, const Dev &D, const ScenConst &C, 
       continue;
     }
     // B6: arrivals with t_arr <= b join the wait tail in (t_arr, id) order
-    while (next_arr <= b) {
-      const int id = D.arr_id[lb + x.arr_head];
-      int pos = x.whead + x.wn;
-      if (pos >= cap) pos -= cap;
-      if (lane == 0) { D.wait_id[lb + pos] = id; D.loc[C.traj_off + id] = L_WAIT; }
-      ++x.wn;
-      ++x.arr_head;
-      next_arr = x.arr_head < x.arr_n ? D.arr_t[lb + x.arr_head] : kInf;
+    if (next_arr <= b) {
+      if (x.wn == 0) { head_ok = false; blocked = false; }
+      do {
+        const int id = D.arr_id[lb + x.arr_head];
+        int pos = x.whead + x.wn;
+        if (pos >= cap) pos -= cap;
+        if (lane == 0) { D.wait_id[lb + pos] = id; D.loc[C.traj_off + id] = L_WAIT; }
+        ++x.wn;
+        ++x.arr_head;
+        next_arr = x.arr_head < x.arr_n ? D.arr_t[lb + x.arr_head] : kInf;
+      } while (next_arr <= b);
+      __syncwarp();
     }
-    __syncwarp();
     // B7: FIFO admission while the head fits the KV budget
-    while (x.wn > 0) {
-      if (!head_ok) {
-        head_id = D.wait_id[lb + x.whead];
-        const long long j = C.traj_off + head_id;
-        head_gen = D.gen[j];
-        head_T = D.T[j];
-        head_ctx = D.prompt[C.grp_off + head_id / P.G] + head_gen;
-        head_ok = true;
+    if (x.wn > 0 && !blocked) {
+      while (x.wn > 0) {
+        if (!head_ok) {
+          head_id = D.wait_id[lb + x.whead];
+          const long long j = C.traj_off + head_id;
+          head_gen = D.gen[j];
+          head_T = D.T[j];
+          head_ctx = D.prompt[C.grp_off + head_id / P.G] + head_gen;
+          head_ok = true;
+        }
+        if (x.kv + k5 * head_ctx > P.M) { blocked = true; break; }
+        if (tail == 32 * kR) {
+          // stable compaction of the live slots through shared memory
+#pragma unroll
+          for (int q = 0; q < kR; ++q) {
+            int before = 0;
+#pragma unroll
+            for (int qq = 0; qq < kR; ++qq)
+              if (qq < q) before += __popc(live[qq]);
+            if ((live[q] >> lane) & 1u) stage[before + __popc(live[q] & lanemask_lt())] = make_int2(rem[q], rid[q]);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int q = 0; q < kR; ++q) {
+            const int s = q * 32 + (int)lane;
+            rem[q] = kDead;
+            if (s < nlive) { const int2 e = stage[s]; rem[q] = e.x; rid[q] = e.y; }
+            live[q] = __ballot_sync(0xffffffffu, s < nlive);
+          }
+          __syncwarp();
+          tail = nlive;
+        }
+        const int s = tail++;
+        const int sq = s >> 5, sl = s & 31;
+#pragma unroll
+        for (int q = 0; q < kR; ++q)
+          if (q == sq) {
+            if ((int)lane == sl) { rem[q] = head_T - head_gen; rid[q] = head_id; }
+            live[q] |= 1u << sl;
+          }
+        if (lane == 0) D.loc[C.traj_off + head_id] = L_RUN;
+        x.kv += k5 * head_ctx;
+        x.prefill += head_ctx;
+        ++nlive;
+        x.whead = x.whead + 1 == cap ? 0 : x.whead + 1;
+        --x.wn;
+        head_ok = false;
       }
-      if (x.kv + k5 * head_ctx > P.M) break;
-      if (tail == 32 * kR) {
-        // stable compaction of the live slots through shared memory
-#pragma unroll
-        for (int q = 0; q < kR; ++q) {
-          int before = 0;
-#pragma unroll
-          for (int qq = 0; qq < kR; ++qq)
-            if (qq < q) before += __popc(live[qq]);
-          if ((live[q] >> lane) & 1u) stage[before + __popc(live[q] & lanemask_lt())] = make_int2(rem[q], rid[q]);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < kR; ++q) {
-          const int s = q * 32 + (int)lane;
-          if (s < nlive) { const int2 e = stage[s]; rem[q] = e.x; rid[q] = e.y; }
-          live[q] = __ballot_sync(0xffffffffu, s < nlive);
-        }
-        __syncwarp();
-        tail = nlive;
-      }
-      const int s = tail++;
-      const int sq = s >> 5, sl = s & 31;
-#pragma unroll
-      for (int q = 0; q < kR; ++q)
-        if (q == sq) {
-          if ((int)lane == sl) { rem[q] = head_T - head_gen; rid[q] = head_id; }
-          live[q] |= 1u << sl;
-        }
-      if (lane == 0) D.loc[C.traj_off + head_id] = L_RUN;
-      x.kv += k5 * head_ctx;
-      x.prefill += head_ctx;
-      ++nlive;
-      x.whead = x.whead + 1 == cap ? 0 : x.whead + 1;
-      --x.wn;
-      head_ok = false;
     }
     // B8: next decode step, Eq 7 + prefill stall (A20)
     if (nlive > 0) {
-      x.nb = b + tick_latency(P, x.kv, nlive, x.prefill);
+      if (nlive != cn_n) { cn_n = nlive; cn = max(P.k2, (long long)P.k3i * nlive) + P.k4; }
+      x.nb = b + (long long)P.k1i * (int)x.kv + cn + (long long)P.kpi * (int)x.prefill;
       x.prefill = 0;
       x.st = I_TICK;
       x.iters += nlive;
       ++x.ticks;
     } else {
       x.st = I_IDLE;
+      continue;
+    }
+    // Quiet decode steps: the next boundary is a step end with no pending command, no
+    // completion (no live rem == 1), no preemption (kv + k5 n <= M), no arrival due, and no
+    // admission possible (B7 just left the head blocked or the queue empty).  Such a boundary
+    // only credits the step (B2) and starts the next one (B8); do exactly that, in registers.
+    if (x.intkind == INT_NONE && !x.pullpend) {
+      const int k5n = (int)(k5 * nlive);
+      for (;;) {
+        const long long bq = x.nb;
+        if (bq > t_end || x.kv + k5n > P.M || next_arr <= bq) break;
+        unsigned one = 0;
+#pragma unroll
+        for (int q = 0; q < kR; ++q) one |= __ballot_sync(0xffffffffu, rem[q] == 1);
+        if (one) break;
+#pragma unroll
+        for (int q = 0; q < kR; ++q) rem[q] -= 1;
+        x.kv += k5n;
+        x.tokens += nlive;
+        x.nb = bq + (long long)P.k1i * (int)x.kv + cn;
+        x.iters += nlive;
+        ++x.ticks;
+      }
     }
   }
   // write the run list back compacted, in admission order

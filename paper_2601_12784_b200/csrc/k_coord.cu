@@ -366,25 +366,28 @@ __device__ int interrupt_victims(const GParams &P, const Dev &D, const ScenConst
   return nvict;
 }
 
-// Order instance i's arrivals by (t_arr, id) (B6): rank sort over the shared-memory route
-// records when they all fit, else over global memory through the free MLQ scratch.
-__device__ void order_arrivals(const GParams &P, const Dev &D, const ScenConst &C, const Cyc &c, Stage &sg,
-                               int n_routed, int i, int n) {
+// Order every instance's arrivals by (t_arr, id) (B6).  All route records of the cycle are
+// staged in shared memory (when they fit): each record's rank among the records of its own
+// instance is its position in that instance's arrival list.  Otherwise rank-sort one instance
+// at a time through global memory and the free MLQ scratch.
+__device__ void order_arrivals_all(const GParams &P, const Dev &D, const ScenConst &C, const Stage &sg, int n_routed) {
+  for (int e = lane_id(); e < n_routed; e += 32) {
+    const int ie = sg.arr_id[e];
+    const long long te = sg.arr_t[e];
+    const int inst = sg.arr_inst[e];
+    int rank = 0;
+    for (int f = 0; f < n_routed; ++f)
+      rank += sg.arr_inst[f] == inst && (sg.arr_t[f] < te || (sg.arr_t[f] == te && sg.arr_id[f] < ie));
+    const long long lb = C.list_off + (long long)inst * C.cap;
+    D.arr_id[lb + rank] = ie;
+    D.arr_t[lb + rank] = te;
+  }
+  __syncwarp();
+}
+
+__device__ void order_arrivals_global(const GParams &P, const Dev &D, const ScenConst &C, const Cyc &c, int i, int n) {
   const unsigned lane = lane_id();
   const long long lb = C.list_off + (long long)i * C.cap;
-  if (n_routed <= kArrStage) {
-    for (int e = lane; e < n_routed; e += 32) {
-      if (sg.arr_inst[e] != i) continue;
-      const long long te = sg.arr_t[e];
-      const int ie = sg.arr_id[e];
-      int rank = 0;
-      for (int f = 0; f < n_routed; ++f)
-        rank += sg.arr_inst[f] == i && (sg.arr_t[f] < te || (sg.arr_t[f] == te && sg.arr_id[f] < ie));
-      D.arr_id[lb + rank] = ie;
-      D.arr_t[lb + rank] = te;
-    }
-    return;
-  }
   int *tmp = D.mlq + C.mlq_off;
   for (int e = lane; e < n; e += 32) {
     const int ie = D.arr_id[lb + e];
@@ -678,13 +681,21 @@ __global__ void __launch_bounds__(128, KS == 1 ? 5 : 2) k_begin_coord(GParams P,
     }
     __syncwarp();
     // order each instance's arrivals by (t_arr, id) for B6
-    for (int i = 0; i < C.I; ++i) {
-      int n = 0;
+    if (nr <= kArrStage) {
+      if (nr > 1) order_arrivals_all(P, D, C, sg, nr);
+      else if (nr == 1 && lane == 0) {
+        const long long lb = C.list_off + (long long)sg.arr_inst[0] * C.cap;
+        D.arr_t[lb] = sg.arr_t[0];
+      }
+    } else {
+      for (int i = 0; i < C.I; ++i) {
+        int n = 0;
 #pragma unroll
-      for (int q = 0; q < KS; ++q)
-        if ((int)lane + 32 * q == i) n = arrn[q];
-      n = __shfl_sync(0xffffffffu, n, i & 31);
-      if (n > 0) order_arrivals(P, D, C, c, sg, nr, i, n);
+        for (int q = 0; q < KS; ++q)
+          if ((int)lane + 32 * q == i) n = arrn[q];
+        n = __shfl_sync(0xffffffffu, n, i & 31);
+        if (n > 0) order_arrivals_global(P, D, C, c, i, n);
+      }
     }
   } else {
     m_invalid = 1;

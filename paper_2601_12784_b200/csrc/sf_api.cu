@@ -141,6 +141,11 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
       cfg->command_log_capacity < 0 || cfg->route_lat_ps < 0 || cfg->pull_lat_ps < 0 || cfg->reward_lat_ps < 0 ||
       cfg->auto_train_windows < 0)
     return SF_E_INVALID;
+  // 32-bit products on the hot path (sf_internal.cuh tick_latency): k1, k3, kp, k5 < 2^31, M < 2^30
+  if (cfg->k1_ps_per_tok < 0 || cfg->k1_ps_per_tok >= (1LL << 31) || cfg->k3_ps < 0 || cfg->k3_ps >= (1LL << 31) ||
+      cfg->kprefill_ps_per_tok < 0 || cfg->kprefill_ps_per_tok >= (1LL << 31) || cfg->kv_budget_tok >= (1LL << 30) ||
+      cfg->k2_ps < 0 || cfg->k4_ps < 0)
+    return SF_E_INVALID;
   sf_ctx *c = new (std::nothrow) sf_ctx();
   if (!c) return SF_E_NOMEM;
   c->device = cfg->device;
@@ -151,6 +156,7 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
   P.B = B; P.G = G;
   P.k1 = cfg->k1_ps_per_tok; P.k2 = cfg->k2_ps; P.k3 = cfg->k3_ps; P.k4 = cfg->k4_ps;
   P.k5 = cfg->k5_tok; P.kp = cfg->kprefill_ps_per_tok; P.M = cfg->kv_budget_tok;
+  P.k1i = (int)P.k1; P.k3i = (int)P.k3; P.kpi = (int)P.kp;
   P.mu = cfg->mu; P.phi_tp = cfg->phi_throughput; P.phi_wait = cfg->phi_wait;
   P.delta = cfg->snap_period_ps; P.r = cfg->route_lat_ps; P.q = cfg->pull_lat_ps; P.R = cfg->reward_lat_ps;
   P.atw = cfg->auto_train_windows; P.pool_cap = cfg->pool_capacity_groups;
