@@ -102,12 +102,6 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def scenario_slice(p, rank, per_gpu):
-    from paper_2601_12784_b200 import workload as W
-    idx = list(range(rank * per_gpu, (rank + 1) * per_gpu))
-    return W.preset_scenario_slice(p, idx), idx
-
-
 def pool_arrays(p, idx, n_groups, group0=0):
     import numpy as np
     from paper_2601_12784_b200 import workload as W
@@ -124,58 +118,62 @@ def run_reference(args, rank, world):
     """The oracle, as it stands, on the host cores: same metric/config, bounded sample."""
     if rank != 0:
         return
-    import numpy as np
-    from oracle.oracle import OracleSim
     from paper_2601_12784_b200 import workload as W
     full = W.preset("C5", n_scenarios=args.scenarios)
-    n_sample = min(32, args.scenarios)
-    idx = list(range(n_sample))
-    o = OracleSim.from_preset(full, idx)
-    for a, k in enumerate(idx):
-        pr, tg = W.draw_lengths(full, k, full.pool_groups)
-        assert o.submit(a, pr, tg) == 0
-    cores = os.cpu_count() or 1
-    o.step(args.warmup, cores)
-    m0 = o.metrics()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        o.step(1, cores)
-    dt = time.perf_counter() - t0
-    it = int(o.metrics()[2] - m0[2])
-    v = it / dt
+    cpu = oracle_rate(full, list(range(args.scenarios)), args.warmup, args.steps, args.cpu_seconds)
+    v = cpu["value"]
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+           "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-           "config": {"workload": f"C5 (sample of {n_sample} of {args.scenarios} scenarios/GPU)",
-                      "scenarios_per_step": n_sample, "windows_per_step": 1},
-           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                            "sample": f"{n_sample} C5 scenarios x {args.steps} windows after {args.warmup} warm-up"},
+           "config": {"workload": f"C5 ({cpu['sample']})", "windows_per_step": 1},
+           "cpu_baseline": cpu,
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
 # ------------------------------------------------------------------------------ cpu baseline
-def cpu_baseline(full, idx_all, warmup, target_s):
+def oracle_rate(full, idx, warmup, steps, target_s, n_first=64):
+    """The oracle (as it stands) on host cores over the SAME window range as the timed GPU
+    region (warm-up windows untimed), on a bounded sample of scenarios sized to ~target_s."""
     from oracle.oracle import OracleSim
     from paper_2601_12784_b200 import workload as W
     cores = os.cpu_count() or 1
-    n_sample = min(64, len(idx_all))
-    idx = idx_all[:n_sample]
-    o = OracleSim.from_preset(full, idx)
-    for a, k in enumerate(idx):
-        pr, tg = W.draw_lengths(full, k, full.pool_groups)
-        assert o.submit(a, pr, tg) == 0
-    o.step(warmup, cores)
-    m0 = o.metrics()
-    t0 = time.perf_counter()
-    windows = 0
-    while time.perf_counter() - t0 < target_s and windows < 400:
-        o.step(1, cores)
-        windows += 1
-    dt = time.perf_counter() - t0
-    it = int(o.metrics()[2] - m0[2])
+    n = min(n_first, len(idx))
+    while True:
+        sample = idx[:n]
+        o = OracleSim.from_preset(full, sample)
+        for a, k in enumerate(sample):
+            pr, tg = W.draw_lengths(full, k, full.pool_groups)
+            assert o.submit(a, pr, tg) == 0
+        o.step(warmup, cores)
+        m0 = o.metrics()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            o.step(1, cores)
+        dt = time.perf_counter() - t0
+        it = int(o.metrics()[2] - m0[2])
+        if dt >= 0.3 * target_s or n >= len(idx):
+            break
+        n = min(len(idx), max(n + 1, int(n * target_s / max(dt, 1e-3))))
     return {"value": it / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{n_sample} C5 scenarios x {windows} windows after {warmup} warm-up ({dt:.1f} s)"}
+            "sample": f"{n} of {len(idx)} C5 scenarios, windows {warmup}..{warmup + steps - 1} "
+                      f"(same range as the timed GPU steps), {dt:.1f} s on {cores} threads"}
+
+
+def shard(n_per_rank: int, rank: int):
+    """Weak scaling: rank r owns scenarios [r*S, (r+1)*S) of one seeded C5 family."""
+    return list(range(rank * n_per_rank, (rank + 1) * n_per_rank))
+
+
+def reduce_metrics(vec, world, dist):
+    """All-reduce of the int64 metrics vector: sums, except slot 30 (max time)."""
+    import torch
+    if world > 1:
+        mx = vec[30].clone()
+        dist.all_reduce(vec, op=dist.ReduceOp.SUM)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        vec[30] = mx
+    return vec
 
 
 # ------------------------------------------------------------------------------ main arm
@@ -199,7 +197,8 @@ def main():
     stream = torch.cuda.current_stream()
     S = args.scenarios
     full = W.preset("C5", n_scenarios=S * world)
-    p, idx = scenario_slice(full, rank, S)
+    idx = shard(S, rank)
+    p = W.preset_scenario_slice(full, idx)
     ctx = StaleFlow.from_preset(p, stream=stream)
     pr, tg = pool_arrays(full, idx, full.pool_groups)
     assert ctx.submit_many(np.arange(S), np.full(S, full.pool_groups), pr, tg) == 0
@@ -237,8 +236,8 @@ def main():
     dm = torch.tensor((m1 - m0).astype(np.int64), device="cuda")
     tm = torch.tensor([ms], dtype=torch.float64, device="cuda")
     adv = torch.tensor([kern_ms[1]], dtype=torch.float64, device="cuda")
+    reduce_metrics(dm, world, dist)                     # the metrics all-reduce (NCCL over NVLink)
     if world > 1:
-        dist.all_reduce(dm, op=dist.ReduceOp.SUM)        # the metrics all-reduce (NCCL over NVLink)
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
         dist.all_reduce(adv, op=dist.ReduceOp.MAX)
     total_iters = int(dm[2].item())
@@ -266,7 +265,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile_run:
-        cpu = cpu_baseline(full, idx, args.warmup, args.cpu_seconds)
+        cpu = oracle_rate(full, idx, args.warmup, args.steps, args.cpu_seconds)
 
     if rank == 0:
         out = {

@@ -13,6 +13,7 @@ LIB = os.path.join(HERE, "libstaleflow.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"]
+FLAGS += [f for f in os.environ.get("SF_NVCC_EXTRA", "").split() if f]
 
 
 def sources():

@@ -14,6 +14,9 @@
 namespace sf {
 
 constexpr int kWarps = 4;      // scenarios per 128-thread block
+#ifndef SF_COORD_MINB
+#define SF_COORD_MINB 5      // blocks per SM for the 1-slot variant (register budget)
+#endif
 constexpr int kArrStage = 128; // route records staged per warp in shared memory
 
 template <int KS>
@@ -33,9 +36,13 @@ struct Cyc {                   // lane-uniform per-cycle scalars
   int cmd_n;
   int reserves;
   int mlq_err;
+  int use_bits;
 };
 
+constexpr int kEmptyWords = 160;   // ledger empty-slot bitmap held in smem when (eta+1)*B <= 5120
+
 struct Stage {                 // per-warp shared-memory staging
+  unsigned empty[kEmptyWords]; // bit s of ring r: slot s of ring buffer r is Empty (valid if use_bits)
   int sfree[kMaxEta + 1];
   int sfree_tmp[kMaxEta + 1];
   int vcnt[kMaxEta + 2];
@@ -147,6 +154,7 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
   for (int k0 = 0; k0 < total && !stop; k0 += 32) {
     // prefetch 32 MLQ items: lane a holds item k0 + a
     int p_id = 0, p_vg = -1, p_l = 0;
+    long long p_ready = 0;
     {
       const int kk = k0 + (int)lane;
       if (kk < total) {
@@ -154,6 +162,7 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
         const int g = p_id / c.G;
         p_vg = D.gv[C.grp_off + g];
         p_l = D.prompt[C.grp_off + g] + D.gen[C.traj_off + p_id];
+        if (tentative < 0) p_ready = D.ready[C.traj_off + p_id];
       }
     }
     const int nb = min(32, total - k0);
@@ -240,11 +249,27 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
           const int ring = b % (c.eta + 1);
           const long long base = C.led_off + (long long)ring * c.B;
           int slot = -1;
-          for (int top = c.B - 1; top >= 0 && slot < 0; top -= 32) {
-            const int sl = top - (int)lane;
-            const bool e = sl >= 0 && D.led_st[base + sl] == E_EMPTY;
-            const unsigned m = __ballot_sync(0xffffffffu, e);
-            if (m) slot = top - (__ffs(m) - 1);
+          if (c.use_bits) {
+            const int bw = (c.B + 31) >> 5;
+            for (int w0 = bw - 1; w0 >= 0 && slot < 0; w0 -= 32) {
+              const int w = w0 - (int)lane;
+              const unsigned word = w >= 0 ? sg.empty[ring * bw + w] : 0u;
+              const unsigned m = __ballot_sync(0xffffffffu, word != 0u);
+              if (m) {
+                const int l = __ffs(m) - 1;
+                const unsigned ww = __shfl_sync(0xffffffffu, word, l);
+                slot = ((w0 - l) << 5) + 31 - __clz(ww);
+              }
+            }
+            __syncwarp();
+            if (lane == 0) sg.empty[ring * bw + (slot >> 5)] &= ~(1u << (slot & 31));
+          } else {
+            for (int top = c.B - 1; top >= 0 && slot < 0; top -= 32) {
+              const int sl = top - (int)lane;
+              const bool e = sl >= 0 && D.led_st[base + sl] == E_EMPTY;
+              const unsigned m = __ballot_sync(0xffffffffu, e);
+              if (m) slot = top - (__ffs(m) - 1);
+            }
           }
           if (lane == 0) {
             D.led_st[base + slot] = E_RESERVED;
@@ -252,7 +277,7 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
             D.led_v[base + slot] = vg;
             D.led_b[C.grp_off + g] = b;
             D.led_s[C.grp_off + g] = slot;
-            D.led_nres[C.ring_off + ring] += 1;
+            atomicAdd(&D.led_nres[C.ring_off + ring], 1);
             D.gv[C.grp_off + g] = vg;
           }
           __syncwarp();
@@ -285,12 +310,13 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
         for (int q = 0; q < KS; ++q)
           if (q == qs) { arrn[q] += 1; acc_delta[q] += 1; }
       }
+      const long long rdy = __shfl_sync(0xffffffffu, p_ready, a);
       if (lane == 0) {
         const long long j = C.traj_off + id;
-        const long long t_arr = max(c.t, D.ready[j]) + P.r;
+        const long long t_arr = max(c.t, rdy) + P.r;
         D.loc[j] = L_TRANSIT;
         D.tinst[j] = (short)sel;
-        D.n_routes[j] += 1;
+        atomicAdd(&D.n_routes[j], 1);
         D.arr_id[C.list_off + (long long)sel * C.cap + aslot] = id;
         if (routed < kArrStage) {
           sg.arr_t[routed] = t_arr;
@@ -353,7 +379,7 @@ __device__ int interrupt_victims(const GParams &P, const Dev &D, const ScenConst
       const long long j = C.traj_off + id;
       D.loc[j] = L_TS;
       D.ready[j] = apply_t;
-      D.n_interrupt[j] += 1;
+      atomicAdd(&D.n_interrupt[j], 1);
       atomicOr(&D.tsv_bits[C.bits_off + (id >> 5)], 1u << (id & 31));
     }
     const int nk = min(32, nvict - k0);
@@ -410,7 +436,7 @@ __device__ void order_arrivals_global(const GParams &P, const Dev &D, const Scen
 }
 
 template <int KS>
-__global__ void __launch_bounds__(128, KS == 1 ? 5 : 2) k_begin_coord(GParams P, Dev D) {
+__global__ void __launch_bounds__(128, KS == 1 ? SF_COORD_MINB : 2) k_begin_coord(GParams P, Dev D) {
   __shared__ Stage stage_all[kWarps];
   const int wib = threadIdx.x >> 5;
   const int s = blockIdx.x * kWarps + wib;
@@ -421,12 +447,17 @@ __global__ void __launch_bounds__(128, KS == 1 ? 5 : 2) k_begin_coord(GParams P,
   if (SS.err) return;
   Stage &sg = stage_all[wib];
   int *sfree = sg.sfree;
+#ifdef SF_TIMING
+  const long long t0_clk = clock64();
+#endif
 
   Cyc c;
   c.t = SS.t; c.cu = SS.cu; c.ps = SS.ps; c.eta = C.eta; c.I = C.I; c.G = P.G; c.B = P.B;
   c.vl_head = SS.vl_head; c.n_ingested = SS.n_ingested; c.window = SS.window; c.min_live_g = SS.min_live_g;
   c.hash = SS.cmd_hash; c.cmd_n = SS.cmd_n; c.reserves = 0; c.mlq_err = 0; c.n_v = 0; c.n_vl = 0;
+  c.use_bits = 0;
   int live = SS.live, err = 0;
+  int dbg_tent = 0;
   long long m_pub = 0, m_batches = 0, m_ingested = 0, m_valid = 0, m_invalid = 0, m_viol = 0;
   long long m_routes = 0, m_interrupts = 0, m_pulls = 0, m_reserves = 0;
   const int nring = C.eta + 1;
@@ -529,6 +560,19 @@ __global__ void __launch_bounds__(128, KS == 1 ? 5 : 2) k_begin_coord(GParams P,
       const int ring = (c.cu + lane) % nring;
       sfree[lane] = P.B - D.led_nres[C.ring_off + ring] - D.led_nocc[C.ring_off + ring];
     }
+    {
+      const int bw = (P.B + 31) >> 5;
+      c.use_bits = nring * bw <= kEmptyWords;
+      if (c.use_bits) {
+        for (int r = 0; r < nring; ++r)
+          for (int w = 0; w < bw; ++w) {
+            const int sl = w * 32 + (int)lane;
+            const bool e = sl < P.B && D.led_st[C.led_off + (long long)r * P.B + sl] == E_EMPTY;
+            const unsigned m = __ballot_sync(0xffffffffu, e);
+            if (lane == 0) sg.empty[r * bw + w] = m;
+          }
+      }
+    }
     __syncwarp();
     const bool vanilla_route = !(C.strategy & 1), vanilla_sync = !(C.strategy & 2), sf_mig = (C.strategy & 4) != 0;
     int min_v = 0x7fffffff;
@@ -565,6 +609,7 @@ __global__ void __launch_bounds__(128, KS == 1 ? 5 : 2) k_begin_coord(GParams P,
 #pragma unroll
           for (int qq = 0; qq < KS; ++qq) { dummy_a[qq] = 0; dummy_b[qq] = 0; }
           Cyc ct = c;
+          ++dbg_tent;
           if (route_pass<KS>(P, D, C, ct, T, sg.sfree_tmp, dummy_a, dummy_b, sg, vanilla_route, i)) keep |= 1u << li;
         }
         selmask[q] = keep;
@@ -717,6 +762,18 @@ __global__ void __launch_bounds__(128, KS == 1 ? 5 : 2) k_begin_coord(GParams P,
     metric_add(SS, M_INTERRUPTS, m_interrupts);
     metric_add(SS, M_PULLS, m_pulls);
     metric_add(SS, M_RESERVES, m_reserves);
+#ifdef SF_TIMING
+    if (D.dbg) {
+      D.dbg[8 * s + 0] = clock64() - t0_clk;
+      D.dbg[8 * s + 1] = m_routes;
+      D.dbg[8 * s + 2] = m_interrupts;
+      D.dbg[8 * s + 3] = m_pulls;
+      D.dbg[8 * s + 4] = m_valid;
+      D.dbg[8 * s + 5] = c.n_v;
+      D.dbg[8 * s + 6] = c.n_vl;
+      D.dbg[8 * s + 7] = dbg_tent;
+    }
+#endif
   }
 }
 

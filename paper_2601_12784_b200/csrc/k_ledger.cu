@@ -96,48 +96,101 @@ __device__ void complete_group(const GParams &P, const Dev &D, const ScenConst &
   ++m_occ;
 }
 
+constexpr int kEvStage = 256;     // reward events staged per warp in shared memory
+
+struct EvStage {
+  long long t[kEvStage];
+  int id[kEvStage];
+  int srt[kEvStage];
+};
+
 __global__ void __launch_bounds__(128) k_ledger(GParams P, Dev D) {
+  __shared__ EvStage stage_all[kWarps];
   const int s = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (s >= P.n_scen) return;
   const unsigned lane = lane_id();
   const ScenConst C = D.sc[s];
   ScenState &SS = D.ss[s];
   if (SS.err) return;
+  EvStage &es = stage_all[threadIdx.x >> 5];
   const long long t_end = SS.t + P.delta;
   const int n = SS.ev_n;
   const int cu = SS.cu;
-  int *tmp = D.mlq + C.mlq_off;                       // scratch (the MLQ is rebuilt per cycle)
   int err = 0;
   long long m_reloc = 0, m_occ = 0;
-  // (t_reward, id) order (W8)
-  for (int e = lane; e < n; e += 32) {
-    const int ie = D.ev_id[C.ev_off + e];
-    const long long te = D.t_complete[C.traj_off + ie];
-    int rank = 0;
-    for (int f = 0; f < n; ++f) {
-      const int jf = D.ev_id[C.ev_off + f];
-      const long long tf = D.t_complete[C.traj_off + jf];
-      rank += (tf < te) || (tf == te && jf < ie);
-    }
-    tmp[rank] = ie;
-  }
-  __syncwarp();
   int np = 0;
-  for (; np < n; ++np) {
-    const int id = tmp[np];
-    if (D.t_complete[C.traj_off + id] + P.R > t_end) break;
-    const int g = id / P.G;
-    const int nr = D.n_rew[C.grp_off + g] + 1;
-    __syncwarp();
-    if (lane == 0) D.n_rew[C.grp_off + g] = nr;
-    __syncwarp();
-    if (nr == P.G) {
-      complete_group(P, D, C, SS, g, cu, m_reloc, m_occ, err);
-      if (err) break;
+  if (n <= kEvStage) {
+    // stage (t_complete, id), rank-sort by (t_reward, id) (W8) in shared memory
+    for (int e = lane; e < n; e += 32) {
+      const int id = D.ev_id[C.ev_off + e];
+      es.id[e] = id;
+      es.t[e] = D.t_complete[C.traj_off + id];
     }
+    __syncwarp();
+    for (int e = lane; e < n; e += 32) {
+      const long long te = es.t[e];
+      const int ie = es.id[e];
+      int rank = 0;
+      for (int f = 0; f < n; ++f) rank += es.t[f] < te || (es.t[f] == te && es.id[f] < ie);
+      es.srt[rank] = e;
+    }
+    __syncwarp();
+    // apply in order, 32 events per batch: the members' reward counters are loaded in parallel and
+    // same-group events inside a batch are counted with __match_any_sync
+    for (int k0 = 0; k0 < n; k0 += 32) {
+      const int k = k0 + (int)lane;
+      const bool valid = k < n;
+      const int e = valid ? es.srt[k] : 0;
+      const int id = es.id[e];
+      const bool ok = valid && es.t[e] + P.R <= t_end;
+      const int g = id / P.G;
+      const unsigned okm = __ballot_sync(0xffffffffu, ok);
+      const int nrw = ok ? D.n_rew[C.grp_off + g] : 0;
+      const unsigned same = __match_any_sync(0xffffffffu, ok ? g : -1 - (int)lane);
+      const int nr = nrw + 1 + __popc(same & lanemask_lt());
+      if (ok && (same >> lane) == 1u) D.n_rew[C.grp_off + g] = nrw + __popc(same);   // last of its group
+      unsigned cm = __ballot_sync(0xffffffffu, ok && nr == P.G);
+      __syncwarp();
+      while (cm) {
+        const int l = __ffs(cm) - 1;
+        cm &= cm - 1;
+        complete_group(P, D, C, SS, __shfl_sync(0xffffffffu, g, l), cu, m_reloc, m_occ, err);
+        if (err) break;
+      }
+      np += __popc(okm);
+      if (err || okm != __ballot_sync(0xffffffffu, valid)) break;   // sorted: the rest are later
+    }
+    __syncwarp();
+    for (int k = np + (int)lane; k < n; k += 32) D.ev_id[C.ev_off + k - np] = es.id[es.srt[k]];
+  } else {
+    int *tmp = D.mlq + C.mlq_off;                     // scratch (the MLQ is rebuilt per cycle)
+    for (int e = lane; e < n; e += 32) {
+      const int ie = D.ev_id[C.ev_off + e];
+      const long long te = D.t_complete[C.traj_off + ie];
+      int rank = 0;
+      for (int f = 0; f < n; ++f) {
+        const int jf = D.ev_id[C.ev_off + f];
+        const long long tf = D.t_complete[C.traj_off + jf];
+        rank += (tf < te) || (tf == te && jf < ie);
+      }
+      tmp[rank] = ie;
+    }
+    __syncwarp();
+    for (; np < n; ++np) {
+      const int id = tmp[np];
+      if (D.t_complete[C.traj_off + id] + P.R > t_end) break;
+      const int g = id / P.G;
+      const int nr = D.n_rew[C.grp_off + g] + 1;
+      __syncwarp();
+      if (lane == 0) D.n_rew[C.grp_off + g] = nr;
+      __syncwarp();
+      if (nr == P.G) {
+        complete_group(P, D, C, SS, g, cu, m_reloc, m_occ, err);
+        if (err) break;
+      }
+    }
+    for (int e = np + (int)lane; e < n; e += 32) D.ev_id[C.ev_off + e - np] = tmp[e];
   }
-  // keep the later events
-  for (int e = np + (int)lane; e < n; e += 32) D.ev_id[C.ev_off + e - np] = tmp[e];
   __syncwarp();
   if (lane == 0) {
     SS.ev_n = n - np;

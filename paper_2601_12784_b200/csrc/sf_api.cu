@@ -215,6 +215,11 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
     sf_destroy(c);
     return SF_E_NOMEM;
   }
+#ifdef SF_TIMING
+  ok = dalloc(c, &D.dbg, 8LL * ns, 0);
+#else
+  D.dbg = nullptr;
+#endif
   D.sc = dsc;
   D.ss = dss;
   D.inst_scen = dinst_scen;
@@ -495,6 +500,15 @@ sf_status sf_dump_instances(sf_ctx *c, int32_t scenario, int64_t *out, int64_t c
 }
 
 int64_t sf_kernel_launches(const sf_ctx *c) { return c ? c->launches : 0; }
+
+#ifdef SF_TIMING
+// debug builds only (-DSF_TIMING): per-scenario coordinator cycles of the last window
+sf_status sf_debug_coord_cycles(sf_ctx *c, int64_t *out) {
+  if (!c || !c->D.dbg) return SF_E_INVALID;
+  cudaMemcpy(out, c->D.dbg, 8 * sizeof(long long) * c->n_scen, cudaMemcpyDeviceToHost);
+  return SF_OK;
+}
+#endif
 
 sf_status sf_profile(sf_ctx *c, int32_t enable) {
   sf_status st = check_ctx(c);

@@ -1,0 +1,76 @@
+"""The C-ABI library builds for sm_100a, loads, and exports every symbol include/staleflow.h
+declares; the Python binding names the same calls.  No compute calls (no GPU here)."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "staleflow.h")
+
+
+def declared_functions():
+    txt = open(HDR).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(sf_[a-z_]+)\s*\(", txt)))
+
+
+@pytest.fixture(scope="module")
+def lib_path():
+    from paper_2601_12784_b200 import build as B
+    return B.build()
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_functions()
+    for must in ("sf_create", "sf_submit_prompts", "sf_step", "sf_publish_params", "sf_collect_batch"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(lib_path):
+    lib = C.CDLL(lib_path)
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+    out = subprocess.run(["nm", "-D", "--defined-only", lib_path], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (sf_[a-z_]+)", out))
+    assert set(declared_functions()) <= exported
+
+
+def test_sm100a_cubin_inside(lib_path):
+    out = subprocess.run(["cuobjdump", "--list-elf", lib_path], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_binding_uses_the_same_names():
+    from paper_2601_12784_b200 import staleflow
+    assert set(staleflow.EXPORTS) == set(declared_functions())
+
+
+def test_binding_refuses_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2601_12784_b200.staleflow import SfError, StaleFlow
+    with pytest.raises(SfError):
+        StaleFlow(4, 1, 8, 64)
+
+
+def test_oracle_is_independent_of_the_product():
+    """The oracle tree includes/imports nothing of the CUDA product and vice versa; the only shared
+    module is the seeded input generator paper_2601_12784_b200/workload.py."""
+    bad_in_oracle = ("staleflow.h", "libstaleflow", "csrc", "paper_2601_12784_b200.staleflow",
+                     "paper_2601_12784_b200 import staleflow")
+    for f in os.listdir(os.path.join(ROOT, "oracle")):
+        if f.endswith((".py", ".cpp", ".h")):
+            src = open(os.path.join(ROOT, "oracle", f)).read()
+            for b in bad_in_oracle:
+                assert b not in src, f"oracle/{f} references {b}"
+    bad_in_product = ("import oracle", "from oracle", "libsforacle", "sf_oracle", "sfo_")
+    for dp, _, fs in os.walk(os.path.join(ROOT, "paper_2601_12784_b200")):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dp, f)).read()
+                for b in bad_in_product:
+                    assert b not in src, f"{f} references {b}"
