@@ -138,7 +138,7 @@ sf_status sf_dump_instances(sf_ctx *ctx, int32_t scenario, int64_t *out, int64_t
 int64_t sf_kernel_launches(const sf_ctx *ctx);
 
 /* Live per-kernel timing: while enabled, sf_step records CUDA events on the context stream
- * around each window kernel (0 coordinate, 1 advance, 2 ledger).  sf_profile_read synchronizes
+ * around each window kernel (0 coordinate, 1 advance, 2 ledger, 3 fused window kernel).  sf_profile_read synchronizes
  * the stream and returns (then resets) the accumulated milliseconds and launch counts in
  * ms[len] / launches[len] (len <= 4). */
 sf_status sf_profile(sf_ctx *ctx, int32_t enable);

@@ -1,0 +1,790 @@
+// k_coord.cu -- window begin + rollout coordinator (DESIGN.md §3.1 W0-W5).
+//
+// One warp per scenario.  The coordinator is inherently sequential over routed trajectories
+// (each Route mutates the snapshot and the ledger, Alg 2), so parallelism is
+// across scenarios (warps) and, inside one decision, across instances: lane l owns instances
+// l, l+32, ... (KS instances per lane, KS = ceil(I/32) chosen at launch so that small-I
+// scenarios keep few registers and high occupancy).  Candidate tests, Eq 3 gains and the
+// waterfall argmax are lane-parallel with deterministic (value, lowest id) warp reductions;
+// fp64 uses only correctly rounded __d*_rn operations so decisions equal the oracle's bit for
+// bit.  Latency: MLQ items are prefetched 32 at a time (one lane each) and route records are
+// staged in shared memory, where each instance's arrivals are ordered by (t_arr, id).
+#pragma once
+#include "sf_internal.cuh"
+
+namespace sf {
+
+constexpr int kCoordWarps = 4; // scenarios per 128-thread block
+#ifndef SF_COORD_MINB
+#define SF_COORD_MINB 5      // blocks per SM for the 1-slot variant (register budget)
+#endif
+constexpr int kArrStage = 128; // route records staged per warp in shared memory
+
+template <int KS>
+struct InstRegs {
+  int v[KS];
+  long long kv[KS];
+  int n[KS];
+  int w[KS];
+};
+
+struct Cyc {                   // lane-uniform per-cycle scalars
+  long long t;
+  int cu, ps, eta, I, G, B;
+  int n_v, n_vl, vl_head, n_ingested, min_live_g;
+  long long window;
+  unsigned long long hash;
+  int cmd_n;
+  int reserves;
+  int mlq_err;
+  int use_bits;
+  int red_w;                   // lanes holding instances (power of 2 >= min(I, 32)): reduction width
+};
+
+constexpr int kEmptyWords = 160;   // ledger empty-slot bitmap held in smem when (eta+1)*B <= 5120
+
+struct Stage {                 // per-warp shared-memory staging
+  unsigned empty[kEmptyWords]; // bit s of ring r: slot s of ring buffer r is Empty (valid if use_bits)
+  int sfree[kMaxEta + 1];
+  int sfree_tmp[kMaxEta + 1];
+  int vcnt[kMaxEta + 2];
+  long long arr_t[kArrStage];
+  int arr_id[kArrStage];
+  short arr_inst[kArrStage];
+  int n_arr;
+};
+
+// verify(v) on the per-warp free counts sfree[d] of buffers cu + d, d in [0, eta].
+__device__ __forceinline__ bool verify_free(const int *sfree, int v, int cu, int eta) {
+  for (int b = v + eta; b >= max(v, cu); --b)
+    if (sfree[b - cu] > 0) return true;
+  return false;
+}
+
+__device__ __forceinline__ void log_cmd(const GParams &P, const Dev &D, const ScenConst &C, Cyc &c, int kind,
+                                        int inst, int traj) {
+  c.hash = fnv_words(c.hash, c.window, kind, inst, traj);
+  if (lane_id() == 0 && c.cmd_n < P.cmdlog_cap) {
+    long long *r = D.cmdlog + C.cmd_off + 4LL * c.cmd_n;
+    r[0] = c.window; r[1] = kind; r[2] = inst; r[3] = traj;
+  }
+  c.cmd_n++;
+}
+
+// Materialise the versioned part of the MLQ (Alg 2 line 2): TS-resident trajectories
+// of versioned groups (TS bitmap, scanned over the live id window) in (v, id) ascending order
+// into D.mlq[mlq_off ...].  Versions lie in [max(0, cu - eta), ps]; items are bucketed stably by
+// version with packed (v - vlo) << 27 | id keys.  Returns the count; *min_v = smallest version
+// present (INT_MAX if none, -1 if an item's version is out of range: protocol bug).
+static __device__ int build_mlq(const Dev &D, const ScenConst &C, const Cyc &c, Stage &sg, int *min_v) {
+  const unsigned lane = lane_id();
+  const int w_lo = (c.min_live_g * c.G) >> 5;
+  const int w_hi = (c.n_ingested * c.G + 31) >> 5;
+  int *tmp = D.mlq + C.mlq_off + C.cap;
+  int *out = D.mlq + C.mlq_off;
+  int n_tmp = 0;
+  for (int w0 = w_lo; w0 < w_hi; w0 += 32) {
+    unsigned word = (w0 + (int)lane < w_hi) ? D.tsv_bits[C.bits_off + w0 + lane] : 0u;
+    const int cnt = __popc(word);
+    const int off = warp_excl_scan(cnt);
+    const int tot = __shfl_sync(0xffffffffu, off + cnt, 31);
+    int pos = n_tmp + off;
+    while (word) {
+      const int b = __ffs(word) - 1;
+      word &= word - 1;
+      tmp[pos++] = ((w0 + (int)lane) << 5) + b;
+    }
+    n_tmp += tot;
+  }
+  *min_v = 0x7fffffff;
+  if (n_tmp == 0) return 0;
+  __syncwarp();
+  const int vlo = max(0, c.cu - c.eta);
+  const int nv = c.ps - vlo + 1;
+  if ((int)lane < kMaxEta + 2) sg.vcnt[lane] = 0;
+  __syncwarp();
+  bool bad = false;
+  for (int k0 = 0; k0 < n_tmp; k0 += 32) {
+    const int k = k0 + (int)lane;
+    if (k < n_tmp) {
+      const int id = tmp[k];
+      const int d = D.gv[C.grp_off + id / c.G] - vlo;
+      if (d < 0 || d >= nv) bad = true;
+      else { tmp[k] = (d << 27) | id; atomicAdd(&sg.vcnt[d], 1); }
+    }
+  }
+  __syncwarp();
+  if (__any_sync(0xffffffffu, bad)) { *min_v = -1; return 0; }
+  int base[kMaxEta + 1];
+  int acc = 0;
+#pragma unroll
+  for (int d = 0; d <= kMaxEta; ++d) {
+    base[d] = acc;
+    if (d < nv) {
+      if (sg.vcnt[d] > 0 && *min_v == 0x7fffffff) *min_v = vlo + d;
+      acc += sg.vcnt[d];
+    }
+  }
+  for (int k0 = 0; k0 < n_tmp; k0 += 32) {
+    const int k = k0 + (int)lane;
+    const int key = k < n_tmp ? tmp[k] : -1;
+    const int dk = key >= 0 ? (key >> 27) : -1;
+#pragma unroll
+    for (int d = 0; d <= kMaxEta; ++d) {
+      if (d >= nv) break;
+      const unsigned m = __ballot_sync(0xffffffffu, dk == d);
+      if (dk == d) out[base[d] + __popc(m & lanemask_lt())] = key & 0x7ffffff;
+      base[d] += __popc(m);
+    }
+  }
+  __syncwarp();
+  return n_tmp;
+}
+
+// One routing pass (Alg 2, or vanilla §6.5) over the MLQ = [versioned n_v items] ++
+// [versionless groups vl_head..n_ingested).  tentative >= 0: Alg 3 trial for that instance on
+// scratch state, returns 1 as soon as a route targets it (early exit allowed).
+// Otherwise issues Route commands and Reserves on the live ledger; returns routes issued.
+template <int KS>
+__device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cyc &c, InstRegs<KS> &S,
+                          int *sfree, int acc_delta[KS], int arrn[KS], Stage &sg, bool vanilla, int tentative) {
+  const unsigned lane = lane_id();
+  const int total = c.n_v + c.n_vl;
+  int pass_group = -1, pass_vg = -1, routed = 0;
+  double Tcur[KS];                                   // Eq 2 of each owned instance's current S
+#pragma unroll
+  for (int q = 0; q < KS; ++q) Tcur[q] = throughput_d(P, S.n[q], S.kv[q]);
+  int k = 0;
+  bool stop = false;
+  for (int k0 = 0; k0 < total && !stop; k0 += 32) {
+    // prefetch 32 MLQ items: lane a holds item k0 + a
+    int p_id = 0, p_vg = -1, p_l = 0;
+    long long p_ready = 0;
+    {
+      const int kk = k0 + (int)lane;
+      if (kk < total) {
+        p_id = kk < c.n_v ? D.mlq[C.mlq_off + kk] : c.vl_head * c.G + (kk - c.n_v);
+        const int g = p_id / c.G;
+        p_vg = D.gv[C.grp_off + g];
+        p_l = D.prompt[C.grp_off + g] + D.gen[C.traj_off + p_id];
+        if (tentative < 0) p_ready = D.ready[C.traj_off + p_id];
+      }
+    }
+    const int nb = min(32, total - k0);
+    for (int a = 0; a < nb; ++a) {
+      k = k0 + a;
+      const int id = __shfl_sync(0xffffffffu, p_id, a);
+      const int g = id / c.G;
+      int vg = __shfl_sync(0xffffffffu, p_vg, a);
+      if (vg < 0 && g == pass_group) vg = pass_vg;
+      const int l = __shfl_sync(0xffffffffu, p_l, a);
+      // Step 1: candidates (check_routable)
+      bool cand[KS];
+      bool any = false;
+#pragma unroll
+      for (int q = 0; q < KS; ++q) {
+        const int i = (int)lane + 32 * q;
+        cand[q] = i < c.I && (vg < 0 ? verify_free(sfree, S.v[q], c.cu, c.eta) : S.v[q] >= vg);
+        any |= cand[q];
+      }
+      if (!__any_sync(0xffffffffu, any)) { stop = true; break; }
+      int sel = -1;
+      if (vanilla) {
+        // fewest trajectories, lowest id
+        long long best = 0x7fffffffffffffffLL;
+#pragma unroll
+        for (int q = 0; q < KS; ++q) {
+          if (!cand[q]) continue;
+          const long long key = ((long long)(S.n[q] + S.w[q]) << 8) | (lane + 32 * q);
+          best = min(best, key);
+        }
+        for (int o = 1; o < c.red_w; o <<= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+        best = __shfl_sync(0xffffffffu, best, 0);
+        sel = (int)(best & 0xff);
+      } else {
+        // Steps 2-4: waterfall over version groups.  One reduction on the
+        // key (lowest version, highest dT, lowest id) yields the best instance of the lowest
+        // remaining version group; accept it if it clears mu * ideal, else retry above that version.
+        const double ideal = ideal_gain_d(P, l);
+        const double thr = __dmul_rn(P.mu, ideal);
+        double dT[KS];
+#pragma unroll
+        for (int q = 0; q < KS; ++q) {
+          dT[q] = 0.0;
+          if (cand[q] && S.w[q] == 0 && S.kv[q] + (long long)P.k5 * l <= P.M)        // gamma (Eq 3)
+            dT[q] = __dsub_rn(throughput_d(P, S.n[q] + 1, S.kv[q] + (long long)P.k5 * l), Tcur[q]);
+        }
+        int last_ver = -1;
+        for (;;) {
+          int bv = 0x7fffffff, bi = 0x7fffffff;
+          double bd = 0.0;
+#pragma unroll
+          for (int q = 0; q < KS; ++q)
+            if (cand[q] && S.v[q] > last_ver &&
+                (S.v[q] < bv || (S.v[q] == bv && dT[q] > bd))) { bv = S.v[q]; bd = dT[q]; bi = (int)lane + 32 * q; }
+          for (int o = 1; o < c.red_w; o <<= 1) {
+            const int ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ov < bv || (ov == bv && (od > bd || (od == bd && oi < bi)))) { bv = ov; bd = od; bi = oi; }
+          }
+          bv = __shfl_sync(0xffffffffu, bv, 0);
+          bd = __shfl_sync(0xffffffffu, bd, 0);
+          bi = __shfl_sync(0xffffffffu, bi, 0);
+          if (bv == 0x7fffffff) break;                     // no group accepted: withhold
+          if (bd >= thr) { sel = bi; break; }              // accept (reading A4)
+          last_ver = bv;
+        }
+      }
+      if (sel < 0) { stop = true; break; }
+      // Step 5: route -- update S (Eq 3), Reserve if the group has no version yet.
+      const int owner = sel & 31, qs = sel >> 5;
+      int sv = 0, sw = 0;
+      long long skv = 0;
+#pragma unroll
+      for (int q = 0; q < KS; ++q)
+        if (q == qs) { sv = S.v[q]; sw = S.w[q]; skv = S.kv[q]; }
+      sv = __shfl_sync(0xffffffffu, sv, owner);
+      sw = __shfl_sync(0xffffffffu, sw, owner);
+      skv = __shfl_sync(0xffffffffu, skv, owner);
+      if (vg < 0) {
+        vg = sv;
+        int b = -1;
+        for (int bb = vg + c.eta; bb >= max(vg, c.cu); --bb)
+          if (sfree[bb - c.cu] > 0) { b = bb; break; }
+        __syncwarp();
+        if (lane == 0) sfree[b - c.cu] -= 1;
+        __syncwarp();
+        if (tentative < 0) {
+          // latest empty slot = highest index in ring buffer b
+          const int ring = b % (c.eta + 1);
+          const long long base = C.led_off + (long long)ring * c.B;
+          int slot = -1;
+          if (c.use_bits) {
+            const int bw = (c.B + 31) >> 5;
+            for (int w0 = bw - 1; w0 >= 0 && slot < 0; w0 -= 32) {
+              const int w = w0 - (int)lane;
+              const unsigned word = w >= 0 ? sg.empty[ring * bw + w] : 0u;
+              const unsigned m = __ballot_sync(0xffffffffu, word != 0u);
+              if (m) {
+                const int l = __ffs(m) - 1;
+                const unsigned ww = __shfl_sync(0xffffffffu, word, l);
+                slot = ((w0 - l) << 5) + 31 - __clz(ww);
+              }
+            }
+            __syncwarp();
+            if (lane == 0) sg.empty[ring * bw + (slot >> 5)] &= ~(1u << (slot & 31));
+          } else {
+            for (int top = c.B - 1; top >= 0 && slot < 0; top -= 32) {
+              const int sl = top - (int)lane;
+              const bool e = sl >= 0 && D.led_st[base + sl] == E_EMPTY;
+              const unsigned m = __ballot_sync(0xffffffffu, e);
+              if (m) slot = top - (__ffs(m) - 1);
+            }
+          }
+          if (lane == 0) {
+            D.led_st[base + slot] = E_RESERVED;
+            D.led_g[base + slot] = g;
+            D.led_v[base + slot] = vg;
+            D.led_b[C.grp_off + g] = b;
+            D.led_s[C.grp_off + g] = slot;
+            atomicAdd(&D.led_nres[C.ring_off + ring], 1);
+            D.gv[C.grp_off + g] = vg;
+          }
+          __syncwarp();
+          c.reserves += 1;
+        }
+        pass_group = g;
+        pass_vg = vg;
+      }
+      const bool gamma = (skv + (long long)P.k5 * l <= P.M) && (sw == 0);
+      if ((int)lane == owner) {
+#pragma unroll
+        for (int q = 0; q < KS; ++q)
+          if (q == qs) {
+            if (gamma) { S.n[q] += 1; S.kv[q] += (long long)P.k5 * l; Tcur[q] = throughput_d(P, S.n[q], S.kv[q]); }
+            else S.w[q] += 1;
+          }
+      }
+      if (tentative >= 0) {
+        if (sel == tentative) return 1;
+        continue;
+      }
+      // issue Route(sel, id): t_arr = t_ready + r (A18)
+      int aslot = 0;
+#pragma unroll
+      for (int q = 0; q < KS; ++q)
+        if (q == qs) aslot = arrn[q];
+      aslot = __shfl_sync(0xffffffffu, aslot, owner);
+      if ((int)lane == owner) {
+#pragma unroll
+        for (int q = 0; q < KS; ++q)
+          if (q == qs) { arrn[q] += 1; acc_delta[q] += 1; }
+      }
+      const long long rdy = __shfl_sync(0xffffffffu, p_ready, a);
+      if (lane == 0) {
+        const long long j = C.traj_off + id;
+        const long long t_arr = max(c.t, rdy) + P.r;
+        D.loc[j] = L_TRANSIT;
+        D.tinst[j] = (short)sel;
+        atomicAdd(&D.n_routes[j], 1);
+        D.arr_id[C.list_off + (long long)sel * C.cap + aslot] = id;
+        if (routed < kArrStage) {
+          sg.arr_t[routed] = t_arr;
+          sg.arr_id[routed] = id;
+          sg.arr_inst[routed] = (short)sel;
+        }
+        if (k < c.n_v) atomicAnd(&D.tsv_bits[C.bits_off + (id >> 5)], ~(1u << (id & 31)));
+      }
+      log_cmd(P, D, C, c, CMD_ROUTE, sel, id);
+      ++routed;
+      if (a == nb - 1) k = k0 + nb;        // pass ran through this batch
+    }
+  }
+  if (tentative >= 0) return 0;
+  if (!stop) k = total;
+  // TS bookkeeping for the versionless range (reading A11)
+  if (k >= total) {
+    c.vl_head = c.n_ingested;
+  } else if (k >= c.n_v) {
+    const int id = c.vl_head * c.G + (k - c.n_v);
+    const int g = id / c.G;
+    if (g == pass_group) {
+      // group versioned in this pass but only partly routed: its other members join the
+      // versioned part of the TS
+      for (int m = id + (int)lane; m < (g + 1) * c.G; m += 32)
+        atomicOr(&D.tsv_bits[C.bits_off + (m >> 5)], 1u << (m & 31));
+      c.vl_head = g + 1;
+    } else {
+      c.vl_head = g;
+    }
+  }
+  __syncwarp();
+  return routed;
+}
+
+// Interrupt (Table 1 row P:573; Alg 1 lines 6-8 / 10-11): victims of instance i are its run list
+// (admission order) then its wait deque entries [w_lo, w_hi) (front -> back order).
+static __device__ int interrupt_victims(const GParams &P, const Dev &D, const ScenConst &C, Cyc &c, int i, bool run_too,
+                                 int w_lo, int w_hi) {
+  const unsigned lane = lane_id();
+  const long long gi = C.inst_off + i;
+  const long long lb = C.list_off + (long long)i * C.cap;
+  const long long apply_t = D.ist[gi] == I_TICK ? D.inb[gi] : c.t;
+  const int nrun = run_too ? D.irun_n[gi] : 0;
+  const int whead = D.iwhead[gi];
+  const int nvict = nrun + (w_hi - w_lo);
+  for (int k0 = 0; k0 < nvict; k0 += 32) {
+    const int k = k0 + (int)lane;
+    int id = -1;
+    if (k < nvict) {
+      if (k < nrun) {
+        id = D.run_id[lb + k];
+        const long long j = C.traj_off + id;
+        D.gen[j] = D.T[j] - D.run_rem[lb + k];       // partial progress kept
+      } else {
+        int pos = whead + w_lo + (k - nrun);
+        if (pos >= C.cap) pos -= C.cap;
+        id = D.wait_id[lb + pos];
+      }
+      const long long j = C.traj_off + id;
+      D.loc[j] = L_TS;
+      D.ready[j] = apply_t;
+      atomicAdd(&D.n_interrupt[j], 1);
+      atomicOr(&D.tsv_bits[C.bits_off + (id >> 5)], 1u << (id & 31));
+    }
+    const int nk = min(32, nvict - k0);
+    for (int a = 0; a < nk; ++a) {
+      const int ida = __shfl_sync(0xffffffffu, id, a);
+      log_cmd(P, D, C, c, CMD_INTERRUPT, i, ida);
+    }
+  }
+  __syncwarp();
+  return nvict;
+}
+
+// Order every instance's arrivals by (t_arr, id) (B6).  All route records of the cycle are
+// staged in shared memory (when they fit): each record's rank among the records of its own
+// instance is its position in that instance's arrival list.  Otherwise rank-sort one instance
+// at a time through global memory and the free MLQ scratch.
+static __device__ void order_arrivals_all(const GParams &P, const Dev &D, const ScenConst &C, const Stage &sg, int n_routed) {
+  for (int e = lane_id(); e < n_routed; e += 32) {
+    const int ie = sg.arr_id[e];
+    const long long te = sg.arr_t[e];
+    const int inst = sg.arr_inst[e];
+    int rank = 0;
+    for (int f = 0; f < n_routed; ++f)
+      rank += sg.arr_inst[f] == inst && (sg.arr_t[f] < te || (sg.arr_t[f] == te && sg.arr_id[f] < ie));
+    const long long lb = C.list_off + (long long)inst * C.cap;
+    D.arr_id[lb + rank] = ie;
+    D.arr_t[lb + rank] = te;
+  }
+  __syncwarp();
+}
+
+static __device__ void order_arrivals_global(const GParams &P, const Dev &D, const ScenConst &C, const Cyc &c, int i, int n) {
+  const unsigned lane = lane_id();
+  const long long lb = C.list_off + (long long)i * C.cap;
+  int *tmp = D.mlq + C.mlq_off;
+  for (int e = lane; e < n; e += 32) {
+    const int ie = D.arr_id[lb + e];
+    const long long te = max(c.t, D.ready[C.traj_off + ie]);
+    int rank = 0;
+    for (int f = 0; f < n; ++f) {
+      const int jf = D.arr_id[lb + f];
+      const long long tf = max(c.t, D.ready[C.traj_off + jf]);
+      rank += (tf < te) || (tf == te && jf < ie);
+    }
+    tmp[rank] = ie;
+  }
+  __syncwarp();
+  for (int e = lane; e < n; e += 32) {
+    const int ie = tmp[e];
+    D.arr_id[lb + e] = ie;
+    D.arr_t[lb + e] = max(c.t, D.ready[C.traj_off + ie]) + P.r;
+  }
+  __syncwarp();
+}
+
+// One window of W0-W5 for scenario s, executed by one warp (sg: that warp's staging).
+template <int KS>
+__device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, int s, Stage &sg) {
+  const unsigned lane = lane_id();
+  const ScenConst C = D.sc[s];
+  ScenState &SS = D.ss[s];
+  if (SS.err) return;
+
+  int *sfree = sg.sfree;
+#ifdef SF_TIMING
+  const long long t0_clk = clock64();
+#endif
+
+  Cyc c;
+  c.t = SS.t; c.cu = SS.cu; c.ps = SS.ps; c.eta = C.eta; c.I = C.I; c.G = P.G; c.B = P.B;
+  c.vl_head = SS.vl_head; c.n_ingested = SS.n_ingested; c.window = SS.window; c.min_live_g = SS.min_live_g;
+  c.hash = SS.cmd_hash; c.cmd_n = SS.cmd_n; c.reserves = 0; c.mlq_err = 0; c.n_v = 0; c.n_vl = 0;
+  c.use_bits = 0;
+  c.red_w = 1;
+  while (c.red_w < min(C.I, 32)) c.red_w <<= 1;
+  int live = SS.live, err = 0;
+  int dbg_tent = 0;
+  long long m_pub = 0, m_batches = 0, m_ingested = 0, m_valid = 0, m_invalid = 0, m_viol = 0;
+  long long m_routes = 0, m_interrupts = 0, m_pulls = 0, m_reserves = 0;
+  const int nring = C.eta + 1;
+
+  // ---------------- W0: auto trainer (reading A24): publish if due, then Consume if Ready
+  if (P.atw > 0) {
+    int busy = SS.trainer_busy;
+    if (busy && SS.publish_at <= c.t) {
+      c.ps += 1;
+      m_pub = 1;
+      busy = 0;
+    }
+    const int ring = c.cu % nring;
+    if (!busy && D.led_nocc[C.ring_off + ring] == P.B) {
+      const long long base = C.led_off + (long long)ring * P.B;
+      const long long bl = C.batch_off + (long long)SS.batch_n * (1 + 2 * P.B);
+      if (lane == 0) D.batches[bl] = c.cu;
+      for (int k = lane; k < P.B; k += 32) {
+        const int g = D.led_g[base + k], v = D.led_v[base + k];
+        D.batches[bl + 1 + 2 * k] = g;
+        D.batches[bl + 2 + 2 * k] = v;
+        const int stal = c.cu - v;                 // staleness V_buf - V_traj (A30)
+        if (stal < 0 || stal > C.eta) { atomicAdd(&SS.m[M_VIOLATIONS], 1ULL); err = ERR_STALENESS; }
+        atomicAdd(&SS.m[M_HIST0 + min(max(stal, 0), 8)], 1ULL);
+        D.cvbuf[C.grp_off + g] = c.cu;
+        for (int m = 0; m < P.G; ++m) D.loc[C.traj_off + (long long)g * P.G + m] = L_CONSUMED;
+        D.led_st[base + k] = E_EMPTY;
+        D.led_g[base + k] = -1;
+        D.led_v[base + k] = -1;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        D.led_nocc[C.ring_off + ring] = 0;
+        D.led_nres[C.ring_off + ring] = 0;
+        SS.batch_n += 1;
+        SS.publish_at = c.t + (long long)P.atw * P.delta;
+      }
+      busy = 1;
+      c.cu += 1;
+      live -= P.B;
+      m_batches = 1;
+    }
+    __syncwarp();
+    if (lane == 0) SS.trainer_busy = busy;
+    err = warp_max(err);
+  }
+  // oldest live group (bounds the TS bitmap scan): skip consumed groups
+  for (;;) {
+    const int g = c.min_live_g + (int)lane;
+    const bool consumed = g < c.n_ingested && D.cvbuf[C.grp_off + g] >= 0;
+    const unsigned m = __ballot_sync(0xffffffffu, !consumed);
+    if (m) { c.min_live_g += __ffs(m) - 1; break; }
+    c.min_live_g += 32;
+  }
+  // ---------------- W1: TS ingest up to (eta+1)*B live groups (A23)
+  {
+    const int n_pool = SS.n_pool;
+    const int room = (C.eta + 1) * P.B - live;
+    const int k = min(room, n_pool - c.n_ingested);
+    if (k > 0) {
+      const long long j0 = C.traj_off + (long long)c.n_ingested * P.G;
+      for (long long a = lane; a < (long long)k * P.G; a += 32) D.loc[j0 + a] = L_TS;
+      c.n_ingested += k;
+      live += k;
+      m_ingested = k;
+    }
+  }
+  __syncwarp();
+  // ---------------- W2: snapshot + Eq 1 (reading R-EQ1)
+  bool ok = true;
+  for (int i = lane; i < C.I; i += 32) {
+    const long long gi = C.inst_off + i;
+    const bool quiescent = D.iintkind[gi] == INT_NONE && !D.ipullpend[gi] && D.iarr_n[gi] == 0 && D.ist[gi] != I_PULL;
+    const bool eq1 = D.ipv[gi] == D.iv[gi] && D.iacc[gi] == D.irun_n[gi] + D.iwn[gi] + D.ic[gi];
+    if (quiescent && !eq1) err = ERR_EQ1;
+    ok &= quiescent && eq1;
+  }
+  err = warp_max(err);
+  if (err == ERR_EQ1) m_viol += 1;
+  const bool valid = __all_sync(0xffffffffu, ok) && !err;
+
+  if (valid) {
+    m_valid = 1;
+    // working snapshot S in registers; ledger free counts of buffers cu..cu+eta in smem
+    InstRegs<KS> S;
+    int acc_delta[KS], arrn[KS];
+#pragma unroll
+    for (int q = 0; q < KS; ++q) {
+      const int i = lane + 32 * q;
+      acc_delta[q] = 0;
+      arrn[q] = 0;
+      if (i < C.I) {
+        const long long gi = C.inst_off + i;
+        S.v[q] = D.iv[gi]; S.kv[q] = D.ikv[gi]; S.n[q] = D.irun_n[gi]; S.w[q] = D.iwn[gi];
+      } else {
+        S.v[q] = 0; S.kv[q] = 0; S.n[q] = 0; S.w[q] = 0;
+      }
+    }
+    if ((int)lane <= C.eta) {
+      const int ring = (c.cu + lane) % nring;
+      sfree[lane] = P.B - D.led_nres[C.ring_off + ring] - D.led_nocc[C.ring_off + ring];
+    }
+    {
+      const int bw = (P.B + 31) >> 5;
+      c.use_bits = nring * bw <= kEmptyWords;
+      if (c.use_bits) {
+        for (int r = 0; r < nring; ++r)
+          for (int w = 0; w < bw; ++w) {
+            const int sl = w * 32 + (int)lane;
+            const bool e = sl < P.B && D.led_st[C.led_off + (long long)r * P.B + sl] == E_EMPTY;
+            const unsigned m = __ballot_sync(0xffffffffu, e);
+            if (lane == 0) sg.empty[r * bw + w] = m;
+          }
+      }
+    }
+    __syncwarp();
+    const bool vanilla_route = !(C.strategy & 1), vanilla_sync = !(C.strategy & 2), sf_mig = (C.strategy & 4) != 0;
+    int min_v = 0x7fffffff;
+    c.n_v = build_mlq(D, C, c, sg, &min_v);
+    if (min_v < 0) c.mlq_err = 1;
+    c.n_vl = (c.n_ingested - c.vl_head) * c.G;
+
+    // ---------------- W3: synchronization (Alg 3; vanilla P:788)
+    unsigned selmask[KS];
+#pragma unroll
+    for (int q = 0; q < KS; ++q) {
+      const int i = lane + 32 * q;
+      bool elig = false;
+      if (i < C.I) {
+        if (vanilla_sync) elig = S.v[q] < c.ps;
+        else elig = c.ps > S.v[q] && !((c.n_vl > 0 && verify_free(sfree, S.v[q], c.cu, c.eta)) ||
+                                       (c.n_v > 0 && min_v <= S.v[q]));
+      }
+      selmask[q] = __ballot_sync(0xffffffffu, elig);
+    }
+    if (!vanilla_sync) {
+#pragma unroll
+      for (int q = 0; q < KS; ++q) {
+        unsigned m = selmask[q], keep = 0;
+        while (m) {
+          const int li = __ffs(m) - 1;
+          m &= m - 1;
+          const int i = li + 32 * q;
+          InstRegs<KS> T = S;
+          if ((int)lane == li) T.v[q] = c.ps;             // S_temp[i].inst_version <- ps
+          if ((int)lane <= C.eta) sg.sfree_tmp[lane] = sfree[lane];
+          __syncwarp();
+          int dummy_a[KS], dummy_b[KS];
+#pragma unroll
+          for (int qq = 0; qq < KS; ++qq) { dummy_a[qq] = 0; dummy_b[qq] = 0; }
+          Cyc ct = c;
+          ++dbg_tent;
+          if (route_pass<KS>(P, D, C, ct, T, sg.sfree_tmp, dummy_a, dummy_b, sg, vanilla_route, i)) keep |= 1u << li;
+        }
+        selmask[q] = keep;
+      }
+    }
+    // apply: Interrupt(i, run u wait) + Pull(i) for each selected i ascending (Alg 1 lines 3-8)
+#pragma unroll
+    for (int q = 0; q < KS; ++q) {
+      unsigned m = selmask[q];
+      while (m) {
+        const int li = __ffs(m) - 1;
+        m &= m - 1;
+        const int i = li + 32 * q;
+        const long long gi = C.inst_off + i;
+        const int nv = interrupt_victims(P, D, C, c, i, true, 0, D.iwn[gi]);
+        if (nv > 0 && lane == 0) { D.iintkind[gi] = INT_ALL; D.iintk[gi] = 0; }
+        m_interrupts += nv;
+        log_cmd(P, D, C, c, CMD_PULL, i, -1);
+        m_pulls += 1;
+        if (lane == 0) {
+          D.ipullpend[gi] = 1;
+          D.ipullv[gi] = c.ps;                 // version delivered = ps at issue (A19)
+          D.ipv[gi] = c.ps;                    // Table 1 Pull row
+          D.iacc[gi] = 0;
+        }
+        if ((int)lane == li) { S.v[q] = c.ps; S.kv[q] = 0; S.n[q] = 0; S.w[q] = 0; acc_delta[q] = 0; }
+        __syncwarp();
+      }
+    }
+    // ---------------- W4: migration (Alg 4), StaleFlow only (vanilla: none)
+    if (sf_mig) {
+      int k1[KS];
+      double Tq[KS];
+#pragma unroll
+      for (int q = 0; q < KS; ++q) {
+        const int i = lane + 32 * q;
+        k1[q] = (i < C.I && S.w[q] > P.phi_wait) ? S.w[q] - P.phi_wait : 0;
+        Tq[q] = throughput_d(P, S.n[q], S.kv[q]);
+      }
+      // argmax / argmin of Eq 2 with lowest-id ties (A9)
+      double tmax = -1.0, tmin = 0.0;
+      int imax = 0x7fffffff, imin = 0x7fffffff;
+#pragma unroll
+      for (int q = 0; q < KS; ++q) {
+        const int i = lane + 32 * q;
+        if (i >= C.I) continue;
+        if (imax == 0x7fffffff || Tq[q] > tmax) { tmax = Tq[q]; imax = i; }
+        if (imin == 0x7fffffff || Tq[q] < tmin) { tmin = Tq[q]; imin = i; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double oa = __shfl_xor_sync(0xffffffffu, tmax, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, imax, o);
+        if (oi != 0x7fffffff && (imax == 0x7fffffff || oa > tmax || (oa == tmax && oi < imax))) { tmax = oa; imax = oi; }
+        const double ob = __shfl_xor_sync(0xffffffffu, tmin, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, imin, o);
+        if (oj != 0x7fffffff && (imin == 0x7fffffff || ob < tmin || (ob == tmin && oj < imin))) { tmin = ob; imin = oj; }
+      }
+      int case2 = -1;
+      if (tmin > 0.0 && __ddiv_rn(tmax, tmin) > P.phi_tp) case2 = imax;      // A5, A6, A8
+      // case 1 (ascending i), then case 2
+#pragma unroll
+      for (int q = 0; q < KS; ++q) {
+        unsigned m = __ballot_sync(0xffffffffu, k1[q] > 0);
+        while (m) {
+          const int li = __ffs(m) - 1;
+          m &= m - 1;
+          const int i = li + 32 * q;
+          const long long gi = C.inst_off + i;
+          const int kk = __shfl_sync(0xffffffffu, k1[q], li);
+          const int wn = D.iwn[gi];
+          const int nv = interrupt_victims(P, D, C, c, i, false, wn - kk, wn);
+          m_interrupts += nv;
+          if (lane == 0) { D.iintkind[gi] = INT_WAIT_TAIL; D.iintk[gi] = kk; D.iacc[gi] -= nv; }
+          if ((int)lane == li) S.w[q] -= kk;
+          __syncwarp();
+        }
+      }
+      if (case2 >= 0) {
+        const int i = case2, q2 = i >> 5, li = i & 31;
+        const long long gi = C.inst_off + i;
+        int kk = 0;
+#pragma unroll
+        for (int qq = 0; qq < KS; ++qq)
+          if (qq == q2) kk = k1[qq];
+        kk = __shfl_sync(0xffffffffu, kk, li);
+        const int wn = D.iwn[gi];
+        const int nv = interrupt_victims(P, D, C, c, i, true, 0, wn - kk);
+        m_interrupts += nv;
+        if (lane == 0) { D.iintkind[gi] = INT_ALL; D.iintk[gi] = 0; D.iacc[gi] -= nv; }
+        if ((int)lane == li) {
+#pragma unroll
+          for (int qq = 0; qq < KS; ++qq)
+            if (qq == q2) { S.kv[qq] = 0; S.n[qq] = 0; S.w[qq] = 0; }
+        }
+        __syncwarp();
+      }
+    }
+    // ---------------- W5: routing (Alg 2) over the TS incl. interrupted trajectories
+    c.n_v = build_mlq(D, C, c, sg, &min_v);
+    if (min_v < 0) c.mlq_err = 1;
+    const int nr = route_pass<KS>(P, D, C, c, S, sfree, acc_delta, arrn, sg, vanilla_route, -1);
+    m_routes = nr;
+    m_reserves = c.reserves;
+    // write back per-instance route effects (Table 1 Route row)
+#pragma unroll
+    for (int q = 0; q < KS; ++q) {
+      const int i = lane + 32 * q;
+      if (i < C.I && (acc_delta[q] || arrn[q])) {
+        const long long gi = C.inst_off + i;
+        D.iacc[gi] += acc_delta[q];
+        D.iarr_n[gi] = arrn[q];
+      }
+    }
+    __syncwarp();
+    // order each instance's arrivals by (t_arr, id) for B6
+    if (nr <= kArrStage) {
+      if (nr > 1) order_arrivals_all(P, D, C, sg, nr);
+      else if (nr == 1 && lane == 0) {
+        const long long lb = C.list_off + (long long)sg.arr_inst[0] * C.cap;
+        D.arr_t[lb] = sg.arr_t[0];
+      }
+    } else {
+      for (int i = 0; i < C.I; ++i) {
+        int n = 0;
+#pragma unroll
+        for (int q = 0; q < KS; ++q)
+          if ((int)lane + 32 * q == i) n = arrn[q];
+        n = __shfl_sync(0xffffffffu, n, i & 31);
+        if (n > 0) order_arrivals_global(P, D, C, c, i, n);
+      }
+    }
+  } else {
+    m_invalid = 1;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    SS.ps = c.ps; SS.cu = c.cu; SS.live = live; SS.n_ingested = c.n_ingested; SS.vl_head = c.vl_head;
+    SS.min_live_g = c.min_live_g;
+    SS.cmd_hash = c.hash; SS.cmd_n = c.cmd_n;
+    if (c.mlq_err) err = ERR_LEDGER;
+    if (err) SS.err = err;
+    metric_add(SS, M_PUBLISHES, m_pub);
+    metric_add(SS, M_BATCHES, m_batches);
+    metric_add(SS, M_INGESTED, m_ingested);
+    metric_add(SS, M_VALID_SNAP, m_valid);
+    metric_add(SS, M_INVALID_SNAP, m_invalid);
+    metric_add(SS, M_VIOLATIONS, m_viol);
+    metric_add(SS, M_ROUTES, m_routes);
+    metric_add(SS, M_INTERRUPTS, m_interrupts);
+    metric_add(SS, M_PULLS, m_pulls);
+    metric_add(SS, M_RESERVES, m_reserves);
+#ifdef SF_TIMING
+    if (D.dbg) {
+      D.dbg[8 * s + 0] = clock64() - t0_clk;
+      D.dbg[8 * s + 1] = m_routes;
+      D.dbg[8 * s + 2] = m_interrupts;
+      D.dbg[8 * s + 3] = m_pulls;
+      D.dbg[8 * s + 4] = m_valid;
+      D.dbg[8 * s + 5] = c.n_v;
+      D.dbg[8 * s + 6] = c.n_vl;
+      D.dbg[8 * s + 7] = dbg_tent;
+    }
+#endif
+  }
+}
+
+}  // namespace sf

@@ -1,455 +1,14 @@
-// k_advance.cu -- decode advance of every rollout instance through one window
-// (DESIGN.md §3.1 W6-W7, boundary procedure §3.2 B1-B8).
-//
-// One warp per instance; instances are independent inside a window (W7), which is the data
-// parallelism of the step.  Fast path (every instance whose run+wait+arrivals fit 32*kR): the
-// instance's run list is staged ONCE per window from HBM into registers -- lane l holds run
-// slots l, l+32, ... with a warp-uniform live bitmask per register row -- and every decode
-// step of the window decrements the remaining-length counters in registers (one token per
-// running trajectory), detects completions with __ballot_sync, and reduces the
-// released KV with warp shuffles only when something completed.  Slot order = admission order,
-// so completions leave holes (compacted lazily through shared memory) and LIFO preemption
-// takes the highest live slot.  The list is written back compacted at the window end.
-// Fallback path: the same procedure streaming the run list through global memory.
-#include "sf_internal.cuh"
+// k_advance.cu -- decode-advance kernel (DESIGN.md §3.1 W6-W7, §3.2 B1-B8): one warp per
+// instance; the per-instance procedure is advance_instance() in advance.cuh.
+#include "advance.cuh"
 
 namespace sf {
-
-constexpr long long kInf = 0x7fffffffffffffffLL;
-constexpr int kR = 4;                      // register rows -> 128 run slots per instance
-constexpr int kWarpsPerBlock = 8;
-
-struct InstState {
-  int st, pullv, pullpend, intkind, intk, cc, v, run_n, whead, wn, arr_n, arr_head;
-  long long nb, until, kv, prefill, t_cmd;
-  long long ticks, iters, tokens, comps, preempts;
-};
-
-__device__ __forceinline__ void emit_completion(const GParams &P, const Dev &D, const ScenConst &C, ScenState &SS,
-                                                int id, long long b, long long &release) {
-  const long long j = C.traj_off + id;
-  const int Tj = D.T[j];
-  release += (long long)P.k5 * (long long)(D.prompt[C.grp_off + id / P.G] + Tj);
-  D.gen[j] = Tj;
-  D.loc[j] = L_DONE;
-  D.t_complete[j] = b;                      // reward due at b + R
-  const int e = atomicAdd(&SS.ev_n, 1);
-  D.ev_id[C.ev_off + e] = id;
-}
-
-// ------------------------------------------------------------------ register-resident path
-// Dead / empty slots hold a sentinel remaining length (kDead) so a decode step is a plain
-// decrement + ballot per register row with no live-mask test; a window has far fewer than kDead
-// steps.  `blocked` records that the wait-queue head did not fit the KV budget and that no KV
-// has been released since (KV only grows on a quiet step), so quiet steps skip B7.
-constexpr int kDead = 1 << 30;
-
-__device__ void advance_reg(const GParams &P, const Dev &D, const ScenConst &C, ScenState &SS, InstState &x,
-                            long long lb, long long t_end, int2 *stage) {
-  const unsigned lane = lane_id();
-  const int cap = C.cap;
-  const long long k5 = P.k5;
-  int rem[kR], rid[kR];
-  unsigned live[kR];
-#pragma unroll
-  for (int q = 0; q < kR; ++q) {
-    const int s = q * 32 + (int)lane;
-    rem[q] = kDead; rid[q] = 0;
-    if (s < x.run_n) { rem[q] = D.run_rem[lb + s]; rid[q] = D.run_id[lb + s]; }
-    live[q] = __ballot_sync(0xffffffffu, s < x.run_n);
-  }
-  int nlive = x.run_n, tail = x.run_n;
-  long long next_arr = x.arr_head < x.arr_n ? D.arr_t[lb + x.arr_head] : kInf;
-  bool head_ok = false, blocked = false;
-  int head_id = 0, head_gen = 0, head_T = 0;
-  long long head_ctx = 0;
-  int cn_n = -1;
-  long long cn = 0;                                   // max(k2, k3 n) + k4 for n = cn_n
-
-  for (;;) {
-    long long b;
-    if (x.st == I_TICK) b = x.nb;
-    else if (x.st == I_PULL) b = x.until;
-    else b = min(x.t_cmd, next_arr);
-    if (b > t_end) break;                             // kInf > t_end
-    x.t_cmd = kInf;
-    const bool tick_end = (x.st == I_TICK);
-    const bool pull_done = (x.st == I_PULL);
-    // B1: pending interrupts leave without this step's token; KV released (A17, A18)
-    if (!pull_done && x.intkind != INT_NONE) {
-      if (x.intkind == INT_ALL) {
-#pragma unroll
-        for (int q = 0; q < kR; ++q) { live[q] = 0u; rem[q] = kDead; }
-        nlive = 0; tail = 0; x.wn = 0; x.kv = 0;
-      } else {
-        x.wn -= x.intk;                                  // wait tail (A7)
-      }
-      if (x.wn == 0) head_ok = false;
-      blocked = false;
-      x.intkind = INT_NONE;
-    }
-    if (tick_end) {
-      // B2 + B3 in registers: one token per running trajectory, ballot the completions
-      const int n0 = nlive;
-      unsigned d[kR], dany = 0;
-#pragma unroll
-      for (int q = 0; q < kR; ++q) {
-        rem[q] -= 1;
-        d[q] = __ballot_sync(0xffffffffu, rem[q] == 0);
-        dany |= d[q];
-      }
-      x.kv += k5 * n0;
-      x.tokens += n0;
-      if (dany) {
-        long long release = 0;
-        int ncomp = 0;
-#pragma unroll
-        for (int q = 0; q < kR; ++q) {
-          if ((d[q] >> lane) & 1u) { emit_completion(P, D, C, SS, rid[q], b, release); rem[q] = kDead; }
-          live[q] &= ~d[q];
-          ncomp += __popc(d[q]);
-        }
-        release = warp_sum(release);
-        x.kv -= release;
-        nlive -= ncomp;
-        x.cc += ncomp;
-        x.comps += ncomp;
-        int t = 0;
-#pragma unroll
-        for (int q = 0; q < kR; ++q)
-          if (live[q]) t = q * 32 + 32 - __clz(live[q]);
-        tail = t;
-        blocked = false;
-      }
-      x.st = I_IDLE;
-    } else if (pull_done) {
-      x.v = x.pullv; x.cc = 0; x.st = I_IDLE;
-    }
-    // B4: preemption while KV exceeds M: newest admitted (highest live slot) -> wait front (A21)
-    if (x.kv > P.M) {
-      while (x.kv > P.M && nlive > 0) {
-        int hq = 0;
-#pragma unroll
-        for (int q = 0; q < kR; ++q)
-          if (live[q]) hq = q;
-        unsigned hm = 0;
-        int r_ = 0, i_ = 0;
-#pragma unroll
-        for (int q = 0; q < kR; ++q)
-          if (q == hq) { hm = live[q]; r_ = rem[q]; i_ = rid[q]; }
-        const int hl = 31 - __clz(hm);
-        const int r = __shfl_sync(0xffffffffu, r_, hl);
-        const int id = __shfl_sync(0xffffffffu, i_, hl);
-        const long long j = C.traj_off + id;
-        const int Tj = D.T[j];
-        const int g_ = Tj - r;
-        const long long ctx = D.prompt[C.grp_off + id / P.G] + g_;
-        x.kv -= k5 * ctx;
-        x.whead = x.whead == 0 ? cap - 1 : x.whead - 1;
-        if (lane == 0) {
-          D.gen[j] = g_;
-          D.loc[j] = L_WAIT;
-          D.n_preempt[j] += 1;
-          D.wait_id[lb + x.whead] = id;
-        }
-#pragma unroll
-        for (int q = 0; q < kR; ++q)
-          if (q == hq) {
-            live[q] &= ~(1u << hl);
-            if ((int)lane == hl) rem[q] = kDead;
-          }
-        --nlive;
-        tail = hq * 32 + hl;
-        ++x.wn;
-        ++x.preempts;
-        head_ok = true; head_id = id; head_gen = g_; head_T = Tj; head_ctx = ctx;
-      }
-      blocked = true;                                 // the last victim (the head) cannot re-fit now
-    }
-    // B5: a pending Pull blocks generation for q
-    if (x.pullpend) {
-      x.pullpend = 0;
-      x.st = I_PULL;
-      x.until = b + P.q;
-      continue;
-    }
-    // B6: arrivals with t_arr <= b join the wait tail in (t_arr, id) order
-    if (next_arr <= b) {
-      if (x.wn == 0) { head_ok = false; blocked = false; }
-      do {
-        const int id = D.arr_id[lb + x.arr_head];
-        int pos = x.whead + x.wn;
-        if (pos >= cap) pos -= cap;
-        if (lane == 0) { D.wait_id[lb + pos] = id; D.loc[C.traj_off + id] = L_WAIT; }
-        ++x.wn;
-        ++x.arr_head;
-        next_arr = x.arr_head < x.arr_n ? D.arr_t[lb + x.arr_head] : kInf;
-      } while (next_arr <= b);
-      __syncwarp();
-    }
-    // B7: FIFO admission while the head fits the KV budget
-    if (x.wn > 0 && !blocked) {
-      while (x.wn > 0) {
-        if (!head_ok) {
-          head_id = D.wait_id[lb + x.whead];
-          const long long j = C.traj_off + head_id;
-          head_gen = D.gen[j];
-          head_T = D.T[j];
-          head_ctx = D.prompt[C.grp_off + head_id / P.G] + head_gen;
-          head_ok = true;
-        }
-        if (x.kv + k5 * head_ctx > P.M) { blocked = true; break; }
-        if (tail == 32 * kR) {
-          // stable compaction of the live slots through shared memory
-#pragma unroll
-          for (int q = 0; q < kR; ++q) {
-            int before = 0;
-#pragma unroll
-            for (int qq = 0; qq < kR; ++qq)
-              if (qq < q) before += __popc(live[qq]);
-            if ((live[q] >> lane) & 1u) stage[before + __popc(live[q] & lanemask_lt())] = make_int2(rem[q], rid[q]);
-          }
-          __syncwarp();
-#pragma unroll
-          for (int q = 0; q < kR; ++q) {
-            const int s = q * 32 + (int)lane;
-            rem[q] = kDead;
-            if (s < nlive) { const int2 e = stage[s]; rem[q] = e.x; rid[q] = e.y; }
-            live[q] = __ballot_sync(0xffffffffu, s < nlive);
-          }
-          __syncwarp();
-          tail = nlive;
-        }
-        const int s = tail++;
-        const int sq = s >> 5, sl = s & 31;
-#pragma unroll
-        for (int q = 0; q < kR; ++q)
-          if (q == sq) {
-            if ((int)lane == sl) { rem[q] = head_T - head_gen; rid[q] = head_id; }
-            live[q] |= 1u << sl;
-          }
-        if (lane == 0) D.loc[C.traj_off + head_id] = L_RUN;
-        x.kv += k5 * head_ctx;
-        x.prefill += head_ctx;
-        ++nlive;
-        x.whead = x.whead + 1 == cap ? 0 : x.whead + 1;
-        --x.wn;
-        head_ok = false;
-      }
-    }
-    // B8: next decode step, Eq 7 + prefill stall (A20)
-    if (nlive > 0) {
-      if (nlive != cn_n) { cn_n = nlive; cn = max(P.k2, (long long)P.k3i * nlive) + P.k4; }
-      x.nb = b + (long long)P.k1i * (int)x.kv + cn + (long long)P.kpi * (int)x.prefill;
-      x.prefill = 0;
-      x.st = I_TICK;
-      x.iters += nlive;
-      ++x.ticks;
-    } else {
-      x.st = I_IDLE;
-      continue;
-    }
-    // Quiet decode steps: the next boundary is a step end with no pending command, no
-    // completion (no live rem == 1), no preemption (kv + k5 n <= M), no arrival due, and no
-    // admission possible (B7 just left the head blocked or the queue empty).  Such a boundary
-    // only credits the step (B2) and starts the next one (B8); do exactly that, in registers.
-    if (x.intkind == INT_NONE && !x.pullpend) {
-      const int k5n = (int)(k5 * nlive);
-      for (;;) {
-        const long long bq = x.nb;
-        if (bq > t_end || x.kv + k5n > P.M || next_arr <= bq) break;
-        unsigned one = 0;
-#pragma unroll
-        for (int q = 0; q < kR; ++q) one |= __ballot_sync(0xffffffffu, rem[q] == 1);
-        if (one) break;
-#pragma unroll
-        for (int q = 0; q < kR; ++q) rem[q] -= 1;
-        x.kv += k5n;
-        x.tokens += nlive;
-        x.nb = bq + (long long)P.k1i * (int)x.kv + cn;
-        x.iters += nlive;
-        ++x.ticks;
-      }
-    }
-  }
-  // write the run list back compacted, in admission order
-  int before = 0;
-#pragma unroll
-  for (int q = 0; q < kR; ++q) {
-    if ((live[q] >> lane) & 1u) {
-      const int pos = before + __popc(live[q] & lanemask_lt());
-      D.run_rem[lb + pos] = rem[q];
-      D.run_id[lb + pos] = rid[q];
-    }
-    before += __popc(live[q]);
-  }
-  x.run_n = nlive;
-}
-
-// ------------------------------------------------------------------ global-memory path
-__device__ void advance_global(const GParams &P, const Dev &D, const ScenConst &C, ScenState &SS, InstState &x,
-                               long long lb, long long t_end) {
-  const unsigned lane = lane_id();
-  const int cap = C.cap;
-  const long long k5 = P.k5;
-  for (;;) {
-    long long b;
-    if (x.st == I_TICK) b = x.nb;
-    else if (x.st == I_PULL) b = x.until;
-    else b = min(x.t_cmd, x.arr_head < x.arr_n ? D.arr_t[lb + x.arr_head] : kInf);
-    if (b == kInf || b > t_end) break;
-    x.t_cmd = kInf;
-    const bool tick_end = (x.st == I_TICK);
-    const bool pull_done = (x.st == I_PULL);
-    if (!pull_done && x.intkind != INT_NONE) {
-      if (x.intkind == INT_ALL) { x.run_n = 0; x.wn = 0; x.kv = 0; }
-      else x.wn -= x.intk;
-      x.intkind = INT_NONE;
-    }
-    if (tick_end) {
-      const int n0 = x.run_n;
-      int out = 0, ncomp = 0;
-      long long release = 0;
-      for (int base = 0; base < n0; base += 32) {
-        const int k = base + (int)lane;
-        const bool valid = k < n0;
-        int rem = 1, id = 0;
-        if (valid) { rem = D.run_rem[lb + k] - 1; id = D.run_id[lb + k]; }
-        const bool done = valid && rem == 0;
-        const bool keep = valid && !done;
-        const unsigned mk = __ballot_sync(0xffffffffu, keep);
-        const unsigned md = __ballot_sync(0xffffffffu, done);
-        const int pos = out + __popc(mk & lanemask_lt());
-        __syncwarp();
-        if (keep) { D.run_rem[lb + pos] = rem; D.run_id[lb + pos] = id; }
-        if (done) emit_completion(P, D, C, SS, id, b, release);
-        out += __popc(mk);
-        ncomp += __popc(md);
-      }
-      if (ncomp) release = warp_sum(release);
-      x.kv += k5 * n0 - release;
-      x.tokens += n0;
-      x.run_n = out;
-      x.cc += ncomp;
-      x.comps += ncomp;
-      x.st = I_IDLE;
-      __syncwarp();
-    }
-    if (pull_done) { x.v = x.pullv; x.cc = 0; x.st = I_IDLE; }
-    while (x.kv > P.M && x.run_n > 0) {
-      const int k = x.run_n - 1;
-      const int id = D.run_id[lb + k];
-      const long long j = C.traj_off + id;
-      const int g_ = D.T[j] - D.run_rem[lb + k];
-      x.kv -= k5 * (long long)(D.prompt[C.grp_off + id / P.G] + g_);
-      x.whead = x.whead == 0 ? cap - 1 : x.whead - 1;
-      if (lane == 0) {
-        D.gen[j] = g_;
-        D.loc[j] = L_WAIT;
-        D.n_preempt[j] += 1;
-        D.wait_id[lb + x.whead] = id;
-      }
-      ++x.wn;
-      --x.run_n;
-      ++x.preempts;
-    }
-    if (x.pullpend) {
-      x.pullpend = 0;
-      x.st = I_PULL;
-      x.until = b + P.q;
-      __syncwarp();
-      continue;
-    }
-    while (x.arr_head < x.arr_n && D.arr_t[lb + x.arr_head] <= b) {
-      const int id = D.arr_id[lb + x.arr_head];
-      int pos = x.whead + x.wn;
-      if (pos >= cap) pos -= cap;
-      if (lane == 0) { D.wait_id[lb + pos] = id; D.loc[C.traj_off + id] = L_WAIT; }
-      ++x.wn;
-      ++x.arr_head;
-    }
-    __syncwarp();
-    while (x.wn > 0) {
-      const int id = D.wait_id[lb + x.whead];
-      const long long j = C.traj_off + id;
-      const int gj = D.gen[j];
-      const long long ctx = D.prompt[C.grp_off + id / P.G] + gj;
-      if (x.kv + k5 * ctx > P.M) break;
-      if (lane == 0) {
-        D.run_id[lb + x.run_n] = id;
-        D.run_rem[lb + x.run_n] = D.T[j] - gj;
-        D.loc[j] = L_RUN;
-      }
-      x.kv += k5 * ctx;
-      x.prefill += ctx;
-      ++x.run_n;
-      x.whead = x.whead + 1 == cap ? 0 : x.whead + 1;
-      --x.wn;
-    }
-    __syncwarp();
-    if (x.run_n > 0) {
-      x.nb = b + tick_latency(P, x.kv, x.run_n, x.prefill);
-      x.prefill = 0;
-      x.st = I_TICK;
-      x.iters += x.run_n;
-      ++x.ticks;
-    } else {
-      x.st = I_IDLE;
-    }
-  }
-}
 
 __global__ void __launch_bounds__(32 * kWarpsPerBlock) k_advance(GParams P, Dev D, int n_inst_total) {
   __shared__ int2 stage_all[kWarpsPerBlock][32 * kR];
   const int gi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (gi >= n_inst_total) return;
-  const unsigned lane = lane_id();
-  const int s = D.inst_scen[gi];
-  const ScenConst C = D.sc[s];
-  ScenState &SS = D.ss[s];
-  if (SS.err) return;
-  const int i = gi - C.inst_off;
-  const long long t = SS.t, t_end = t + P.delta;
-  const long long lb = C.list_off + (long long)i * C.cap;
-
-  InstState x;
-  x.st = D.ist[gi]; x.nb = D.inb[gi]; x.until = D.iuntil[gi];
-  x.pullv = D.ipullv[gi]; x.pullpend = D.ipullpend[gi];
-  x.intkind = D.iintkind[gi]; x.intk = D.iintk[gi];
-  x.kv = D.ikv[gi]; x.prefill = D.iprefill[gi]; x.cc = D.ic[gi]; x.v = D.iv[gi];
-  x.run_n = D.irun_n[gi]; x.whead = D.iwhead[gi]; x.wn = D.iwn[gi];
-  x.arr_n = D.iarr_n[gi]; x.arr_head = 0;
-  x.ticks = x.iters = x.tokens = x.comps = x.preempts = 0;
-  // W6: commands to an idle instance apply at a boundary at t
-  x.t_cmd = (x.st == I_IDLE && (x.pullpend || x.intkind != INT_NONE)) ? t : kInf;
-
-  if (x.run_n + x.wn + x.arr_n <= 32 * kR) advance_reg(P, D, C, SS, x, lb, t_end, stage_all[threadIdx.x >> 5]);
-  else advance_global(P, D, C, SS, x, lb, t_end);
-
-  // keep undelivered arrivals (held while pulling / later than the window) at the list front
-  const int remain = x.arr_n - x.arr_head;
-  if (x.arr_head > 0 && remain > 0) {
-    for (int k0 = 0; k0 < remain; k0 += 32) {
-      const int k = k0 + (int)lane;
-      long long ta = 0;
-      int ia = 0;
-      if (k < remain) { ta = D.arr_t[lb + x.arr_head + k]; ia = D.arr_id[lb + x.arr_head + k]; }
-      __syncwarp();
-      if (k < remain) { D.arr_t[lb + k] = ta; D.arr_id[lb + k] = ia; }
-      __syncwarp();
-    }
-  }
-  if (lane == 0) {
-    D.ist[gi] = x.st; D.inb[gi] = x.nb; D.iuntil[gi] = x.until;
-    D.ipullpend[gi] = x.pullpend; D.iintkind[gi] = x.intkind;
-    D.ikv[gi] = x.kv; D.iprefill[gi] = x.prefill; D.ic[gi] = x.cc; D.iv[gi] = x.v;
-    D.irun_n[gi] = x.run_n; D.iwhead[gi] = x.whead; D.iwn[gi] = x.wn; D.iarr_n[gi] = remain;
-    metric_add(SS, M_TICKS, x.ticks);
-    metric_add(SS, M_TRAJ_ITERS, x.iters);
-    metric_add(SS, M_TOKENS, x.tokens);
-    metric_add(SS, M_COMPLETIONS, x.comps);
-    metric_add(SS, M_PREEMPTIONS, x.preempts);
-  }
+  advance_instance(P, D, gi, stage_all[threadIdx.x >> 5]);
 }
 
 }  // namespace sf

@@ -1,206 +1,14 @@
-// k_ledger.cu -- reward events -> staleness ledger (DESIGN.md §3.1 W8-W9, §3.3), external
-// Consume, metric reduction and dump kernels.
-//
-// One warp per scenario.  Reward events of the window are put in (t_reward, trajectory id)
-// order with a warp rank sort (keys t_complete + R, id), then applied in that order: mark the
-// member; once the whole GRPO group is rewarded delete its Reserved entry and cascade
-// earlier Reserved entries into the hole, then Occupy the earliest empty slot
-// (P:366).  Slot searches are warp ballots over 32 slots at a time.
-#include "sf_internal.cuh"
+// k_ledger.cu -- reward -> ledger kernel (DESIGN.md §3.1 W8-W9; procedure ledger_scenario() in
+// ledger.cuh), external Consume, metric reduction, dump and pool-scatter kernels.
+#include "ledger.cuh"
 
 namespace sf {
 
-constexpr int kWarps = 4;
-
-__device__ __forceinline__ long long ring_base(const ScenConst &C, int B, int b) {
-  return C.led_off + (long long)(b % (C.eta + 1)) * B;
-}
-
-// lowest slot index in [0, B) of ring buffer b satisfying pred (warp ballot), or -1
-template <typename Pred>
-__device__ __forceinline__ int first_slot(int B, Pred pred) {
-  for (int s0 = 0; s0 < B; s0 += 32) {
-    const int sl = s0 + (int)lane_id();
-    const bool h = sl < B && pred(sl);
-    const unsigned m = __ballot_sync(0xffffffffu, h);
-    if (m) return s0 + __ffs(m) - 1;
-  }
-  return -1;
-}
-
-__device__ void complete_group(const GParams &P, const Dev &D, const ScenConst &C, ScenState &SS, int g, int cu,
-                               long long &m_reloc, long long &m_occ, int &err) {
-  const unsigned lane = lane_id();
-  const int B = P.B, eta = C.eta;
-  int hb = D.led_b[C.grp_off + g], hs = D.led_s[C.grp_off + g];
-  const int vg = D.gv[C.grp_off + g];
-  {
-    const long long base = ring_base(C, B, hb);
-    if (D.led_st[base + hs] != E_RESERVED || D.led_g[base + hs] != g) { err = ERR_LEDGER; return; }
-    __syncwarp();
-    if (lane == 0) {
-      D.led_st[base + hs] = E_EMPTY; D.led_g[base + hs] = -1; D.led_v[base + hs] = -1;
-      D.led_nres[C.ring_off + hb % (eta + 1)] -= 1;
-    }
-    __syncwarp();
-  }
-  // delete-and-relocate cascade (reading A13)
-  for (;;) {
-    int fb = -1, fs = -1;
-    for (int bb = cu; bb < hb; ++bb) {
-      if (D.led_nres[C.ring_off + bb % (eta + 1)] == 0) continue;
-      const long long base = ring_base(C, B, bb);
-      const int hole = hb;
-      const int sl = first_slot(B, [&](int x) {
-        return D.led_st[base + x] == E_RESERVED && D.led_v[base + x] + eta >= hole;
-      });
-      if (sl >= 0) { fb = bb; fs = sl; break; }
-    }
-    if (fb < 0) break;
-    const long long src = ring_base(C, B, fb) + fs, dst = ring_base(C, B, hb) + hs;
-    const int mg = D.led_g[src], mv = D.led_v[src];
-    __syncwarp();
-    if (lane == 0) {
-      D.led_st[dst] = E_RESERVED; D.led_g[dst] = mg; D.led_v[dst] = mv;
-      D.led_st[src] = E_EMPTY; D.led_g[src] = -1; D.led_v[src] = -1;
-      D.led_nres[C.ring_off + hb % (eta + 1)] += 1;
-      D.led_nres[C.ring_off + fb % (eta + 1)] -= 1;
-      D.led_b[C.grp_off + mg] = hb;
-      D.led_s[C.grp_off + mg] = hs;
-    }
-    __syncwarp();
-    hb = fb;
-    hs = fs;
-    ++m_reloc;
-  }
-  // Occupy: earliest buffer >= cu with an empty slot, lowest slot
-  int ob = -1, os = -1;
-  for (int b = cu; b <= cu + eta; ++b) {
-    const int r = C.ring_off + b % (eta + 1);
-    if (B - D.led_nres[r] - D.led_nocc[r] <= 0) continue;
-    const long long base = ring_base(C, B, b);
-    os = first_slot(B, [&](int x) { return D.led_st[base + x] == E_EMPTY; });
-    if (os >= 0) { ob = b; break; }
-  }
-  if (ob < 0) { err = ERR_LEDGER; return; }
-  if (ob < vg || ob > vg + eta) { err = ERR_STALENESS; atomicAdd(&SS.m[M_VIOLATIONS], lane == 0 ? 1ULL : 0ULL); }
-  __syncwarp();
-  if (lane == 0) {
-    const long long dst = ring_base(C, B, ob) + os;
-    D.led_st[dst] = E_OCCUPIED; D.led_g[dst] = g; D.led_v[dst] = vg;
-    D.led_nocc[C.ring_off + ob % (eta + 1)] += 1;
-    D.led_b[C.grp_off + g] = ob;
-    D.led_s[C.grp_off + g] = os;
-  }
-  __syncwarp();
-  ++m_occ;
-}
-
-constexpr int kEvStage = 256;     // reward events staged per warp in shared memory
-
-struct EvStage {
-  long long t[kEvStage];
-  int id[kEvStage];
-  int srt[kEvStage];
-};
-
 __global__ void __launch_bounds__(128) k_ledger(GParams P, Dev D) {
-  __shared__ EvStage stage_all[kWarps];
-  const int s = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  __shared__ EvStage stage_all[kLedgerWarps];
+  const int s = blockIdx.x * kLedgerWarps + (threadIdx.x >> 5);
   if (s >= P.n_scen) return;
-  const unsigned lane = lane_id();
-  const ScenConst C = D.sc[s];
-  ScenState &SS = D.ss[s];
-  if (SS.err) return;
-  EvStage &es = stage_all[threadIdx.x >> 5];
-  const long long t_end = SS.t + P.delta;
-  const int n = SS.ev_n;
-  const int cu = SS.cu;
-  int err = 0;
-  long long m_reloc = 0, m_occ = 0;
-  int np = 0;
-  if (n <= kEvStage) {
-    // stage (t_complete, id), rank-sort by (t_reward, id) (W8) in shared memory
-    for (int e = lane; e < n; e += 32) {
-      const int id = D.ev_id[C.ev_off + e];
-      es.id[e] = id;
-      es.t[e] = D.t_complete[C.traj_off + id];
-    }
-    __syncwarp();
-    for (int e = lane; e < n; e += 32) {
-      const long long te = es.t[e];
-      const int ie = es.id[e];
-      int rank = 0;
-      for (int f = 0; f < n; ++f) rank += es.t[f] < te || (es.t[f] == te && es.id[f] < ie);
-      es.srt[rank] = e;
-    }
-    __syncwarp();
-    // apply in order, 32 events per batch: the members' reward counters are loaded in parallel and
-    // same-group events inside a batch are counted with __match_any_sync
-    for (int k0 = 0; k0 < n; k0 += 32) {
-      const int k = k0 + (int)lane;
-      const bool valid = k < n;
-      const int e = valid ? es.srt[k] : 0;
-      const int id = es.id[e];
-      const bool ok = valid && es.t[e] + P.R <= t_end;
-      const int g = id / P.G;
-      const unsigned okm = __ballot_sync(0xffffffffu, ok);
-      const int nrw = ok ? D.n_rew[C.grp_off + g] : 0;
-      const unsigned same = __match_any_sync(0xffffffffu, ok ? g : -1 - (int)lane);
-      const int nr = nrw + 1 + __popc(same & lanemask_lt());
-      if (ok && (same >> lane) == 1u) D.n_rew[C.grp_off + g] = nrw + __popc(same);   // last of its group
-      unsigned cm = __ballot_sync(0xffffffffu, ok && nr == P.G);
-      __syncwarp();
-      while (cm) {
-        const int l = __ffs(cm) - 1;
-        cm &= cm - 1;
-        complete_group(P, D, C, SS, __shfl_sync(0xffffffffu, g, l), cu, m_reloc, m_occ, err);
-        if (err) break;
-      }
-      np += __popc(okm);
-      if (err || okm != __ballot_sync(0xffffffffu, valid)) break;   // sorted: the rest are later
-    }
-    __syncwarp();
-    for (int k = np + (int)lane; k < n; k += 32) D.ev_id[C.ev_off + k - np] = es.id[es.srt[k]];
-  } else {
-    int *tmp = D.mlq + C.mlq_off;                     // scratch (the MLQ is rebuilt per cycle)
-    for (int e = lane; e < n; e += 32) {
-      const int ie = D.ev_id[C.ev_off + e];
-      const long long te = D.t_complete[C.traj_off + ie];
-      int rank = 0;
-      for (int f = 0; f < n; ++f) {
-        const int jf = D.ev_id[C.ev_off + f];
-        const long long tf = D.t_complete[C.traj_off + jf];
-        rank += (tf < te) || (tf == te && jf < ie);
-      }
-      tmp[rank] = ie;
-    }
-    __syncwarp();
-    for (; np < n; ++np) {
-      const int id = tmp[np];
-      if (D.t_complete[C.traj_off + id] + P.R > t_end) break;
-      const int g = id / P.G;
-      const int nr = D.n_rew[C.grp_off + g] + 1;
-      __syncwarp();
-      if (lane == 0) D.n_rew[C.grp_off + g] = nr;
-      __syncwarp();
-      if (nr == P.G) {
-        complete_group(P, D, C, SS, g, cu, m_reloc, m_occ, err);
-        if (err) break;
-      }
-    }
-    for (int e = np + (int)lane; e < n; e += 32) D.ev_id[C.ev_off + e - np] = tmp[e];
-  }
-  __syncwarp();
-  if (lane == 0) {
-    SS.ev_n = n - np;
-    SS.t = t_end;                                       // W9
-    SS.window += 1;
-    if (err) SS.err = err;
-    metric_add(SS, M_WINDOWS, 1);
-    metric_add(SS, M_RELOCATIONS, m_reloc);
-    metric_add(SS, M_OCCUPIED, m_occ);
-  }
+  ledger_scenario(P, D, s, stage_all[threadIdx.x >> 5]);
 }
 
 // External-trainer Consume for one scenario; out[0] = status (0 ok, 1 not ready),
@@ -307,7 +115,7 @@ __global__ void k_scatter_pool(Dev D, int G, const int *desc, int n_desc, const 
 }  // namespace sf
 
 void sf_launch_ledger(const sf::GParams &P, const sf::Dev &D, int n_scen, cudaStream_t st) {
-  sf::k_ledger<<<(n_scen + sf::kWarps - 1) / sf::kWarps, 128, 0, st>>>(P, D);
+  sf::k_ledger<<<(n_scen + sf::kLedgerWarps - 1) / sf::kLedgerWarps, 128, 0, st>>>(P, D);
 }
 void sf_launch_collect(const sf::GParams &P, const sf::Dev &D, int scen, int *out_dev, cudaStream_t st) {
   sf::k_collect<<<1, 32, 0, st>>>(P, D, scen, out_dev);

@@ -1,0 +1,48 @@
+// k_window.cu -- fused window kernel for many small scenarios (DESIGN.md §8 "launch modes").
+//
+// Scenarios are independent, so one warp can run its scenario's whole window -- coordinator
+// (W0-W5), the decode advance of each of its instances (W6-W7), then the reward ledger (W8-W9)
+// -- with no grid-wide barrier between the phases.  Latency-bound coordinator work of one
+// scenario then overlaps with other warps' decode steps on the same SM instead of every phase
+// waiting for the slowest scenario, and several windows can run in one launch.  Used when every
+// scenario has few instances (the per-warp serial advance stays short); the three-kernel path
+// (k_begin_coord / k_advance / k_ledger) handles large instance counts.
+#include "advance.cuh"
+#include "coord.cuh"
+#include "ledger.cuh"
+
+namespace sf {
+
+constexpr int kFusedWarps = 4;
+
+union WinStage {
+  Stage coord;
+  int2 adv[32 * kR];
+  EvStage led;
+};
+
+template <int KS>
+__global__ void __launch_bounds__(32 * kFusedWarps) k_window(GParams P, Dev D, int n_windows) {
+  __shared__ WinStage st_all[kFusedWarps];
+  const int s = blockIdx.x * kFusedWarps + (threadIdx.x >> 5);
+  if (s >= P.n_scen) return;
+  WinStage &ws = st_all[threadIdx.x >> 5];
+  const int inst_off = D.sc[s].inst_off, I = D.sc[s].I;
+  for (int w = 0; w < n_windows; ++w) {
+    coord_scenario<KS>(P, D, s, ws.coord);
+    __syncwarp();
+    for (int i = 0; i < I; ++i) advance_instance(P, D, inst_off + i, ws.adv);
+    __syncwarp();
+    ledger_scenario(P, D, s, ws.led);
+    __syncwarp();
+  }
+}
+
+}  // namespace sf
+
+void sf_launch_window_fused(const sf::GParams &P, const sf::Dev &D, int n_scen, int max_inst, int n_windows,
+                            cudaStream_t st) {
+  const int blocks = (n_scen + sf::kFusedWarps - 1) / sf::kFusedWarps;
+  (void)max_inst;                       // fused mode requires <= 32 instances (sf_api.cu)
+  sf::k_window<1><<<blocks, 32 * sf::kFusedWarps, 0, st>>>(P, D, n_windows);
+}

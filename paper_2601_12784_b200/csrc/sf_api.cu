@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -24,6 +25,7 @@ struct sf_ctx {
   std::vector<int> hn_pool;
   int n_inst_total = 0;
   int max_inst = 1;
+  int fused = 0;                      // launch mode: 1 = one fused window kernel (k_window)
   int n_scen = 0;
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -186,6 +188,13 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
     bits += bwords; mlq += 2LL * S.cap; ev += S.cap; batch += batch_rec; cmd += 4LL * P.cmdlog_cap;
   }
   c->n_inst_total = (int)inst;
+  // launch mode: the three-kernel path by default (measured faster on C5);
+  // SF_LAUNCH=fused selects the fused per-scenario window kernel (tests run both)
+  c->fused = 0;
+  if (const char *m = getenv("SF_LAUNCH")) {
+    if (!strcmp(m, "split")) c->fused = 0;
+    if (!strcmp(m, "fused")) c->fused = c->max_inst <= 32;
+  }
   const long long ntraj = (long long)ns * pool_traj, ngrp = (long long)ns * P.pool_cap;
   Dev &D = c->D;
   bool ok = true;
@@ -310,7 +319,13 @@ sf_status sf_step(sf_ctx *c, int32_t n_windows, sf_step_stats *out) {
   if (n_windows < 0) return fail(c, SF_E_INVALID, "n_windows < 0");
   long long before[sf::kMetrics] = {0}, after[sf::kMetrics] = {0};
   if (out && (st = reduce_metrics_host(c, before)) != SF_OK) return st;
-  for (int w = 0; w < n_windows; ++w) {
+  if (c->fused && n_windows > 0) {
+    prof_mark(c, 3);
+    sf_launch_window_fused(c->P, c->D, c->n_scen, c->max_inst, n_windows, c->stream);
+    prof_mark(c, 3);
+    c->launches += 1;
+  }
+  for (int w = 0; w < (c->fused ? 0 : n_windows); ++w) {
     prof_mark(c, 0);
     sf_launch_begin_coord(c->P, c->D, c->n_scen, c->max_inst, c->stream);
     prof_mark(c, 0);

@@ -16,6 +16,16 @@ from tests.parity import compare, make_pair, run_lockstep, submit_both
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["auto", "fused"])
+def launch_mode(request, monkeypatch):
+    """Both launch modes (three kernels / fused window kernel) must give identical results."""
+    if request.param != "auto":
+        monkeypatch.setenv("SF_LAUNCH", request.param)
+    else:
+        monkeypatch.delenv("SF_LAUNCH", raising=False)
+    return request.param
+
+
 def gpu_from_config(I, eta, G, cfg, cmdlog=100_000):
     from paper_2601_12784_b200.staleflow import StaleFlow
     return StaleFlow(I, eta, G, cfg.batch_size, 1, k1=cfg.k1, k2=cfg.k2, k3=cfg.k3, k4=cfg.k4, k5=cfg.k5,
@@ -25,7 +35,7 @@ def gpu_from_config(I, eta, G, cfg, cmdlog=100_000):
                      command_log_capacity=cmdlog)
 
 
-def test_T1_on_gpu():
+def test_T1_on_gpu(launch_mode):
     cfg = Config(batch_size=1, n_scenarios=1, k1=1, k2=100, k3=10, k4=50, k5=1, kp=0, M=1000, mu=0.3,
                  phi_tp=5.0, phi_wait=3, delta=1000, r=5, q=30, R=20, strategy=7, atw=1, pool_capacity_groups=4)
     o = OracleSim(1, 0, 2, cfg)
@@ -42,7 +52,7 @@ def _fuzz_config(rng):
 
 
 @pytest.mark.parametrize("seed", range(24))
-def test_fuzz_small_configs(seed):
+def test_fuzz_small_configs(seed, launch_mode):
     rng = random.Random(seed)
     I, eta, G, cfg, prompt, target, steps = _fuzz_config(rng)
     o = OracleSim(I, eta, G, cfg)
@@ -59,7 +69,7 @@ def test_empty_pool_and_no_work():
     assert g.metrics()[2] == 0
 
 
-def test_external_trainer_collect_publish():
+def test_external_trainer_collect_publish(launch_mode):
     """External mode (atw = 0): the caller Consumes and Pushes."""
     import dataclasses
     p = dataclasses.replace(W.preset("C1"), auto_train_windows=0)
@@ -79,7 +89,7 @@ def test_external_trainer_collect_publish():
 
 
 @pytest.mark.parametrize("name,windows,every", [("C1", 400, 25), ("C3", 120, 30), ("C2", 80, 40)])
-def test_single_scenario_presets(name, windows, every):
+def test_single_scenario_presets(name, windows, every, launch_mode):
     p = W.preset(name)
     o, g = make_pair(p)
     submit_both(o, g, p)
@@ -94,7 +104,7 @@ def test_c4_subset():
     run_lockstep(o, g, list(range(len(idx))), 60, every=30)
 
 
-def test_c5_full_size_sampled():
+def test_c5_full_size_sampled(launch_mode):
     """C5 at full size (4096 scenarios, bench launch configuration) on the GPU; a seeded sample
     of scenarios is recomputed one by one by the oracle (scenarios are independent)."""
     from paper_2601_12784_b200.staleflow import StaleFlow
