@@ -30,7 +30,7 @@ __device__ __forceinline__ void emit_completion(const GParams &P, const Dev &D, 
                                                 int id, long long b, long long &release) {
   const long long j = C.traj_off + id;
   const int Tj = D.T[j];
-  release += (long long)P.k5 * (long long)(D.prompt[C.grp_off + id / P.G] + Tj);
+  release += (long long)P.k5 * (long long)(D.prompt[C.grp_off + grp_of(P, id)] + Tj);
   D.gen[j] = Tj;
   D.loc[j] = L_DONE;
   D.t_complete[j] = b;                      // reward due at b + R
@@ -41,25 +41,59 @@ __device__ __forceinline__ void emit_completion(const GParams &P, const Dev &D, 
 // ------------------------------------------------------------------ register-resident path
 // Dead / empty slots hold a sentinel remaining length (kDead) so a decode step is a plain
 // decrement + ballot per register row with no live-mask test; a window has far fewer than kDead
-// steps.  `blocked` records that the wait-queue head did not fit the KV budget and that no KV
-// has been released since (KV only grows on a quiet step), so quiet steps skip B7.
+// steps.  Every live slot also keeps its trajectory's target T and final context p + T in
+// registers, so completions and preemptions need no memory loads; completion events are
+// buffered in shared memory and reserved in the scenario's event list with one atomic per
+// flush.  Up to 32 pending arrivals are prefetched (id, gen, T, prompt) into lanes so that
+// admitting them reads registers.  `blocked` records that the wait head did not fit the KV
+// budget and no KV was released since (KV only grows on a quiet step), so quiet steps skip B7.
 constexpr int kDead = 1 << 30;
+constexpr int kEvBuf = 32 * kR;           // completion events buffered per warp
+
+struct AdvStage {
+  int4 compact[32 * kR];                  // (rem, id, T, p + T) during slot compaction
+  int ev[kEvBuf];
+};
+
+__device__ __forceinline__ void flush_events(const Dev &D, const ScenConst &C, ScenState &SS, const int *ev, int &n) {
+  if (n == 0) return;
+  int base = 0;
+  if (lane_id() == 0) base = atomicAdd(&SS.ev_n, n);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (int k = lane_id(); k < n; k += 32) D.ev_id[C.ev_off + base + k] = ev[k];
+  __syncwarp();
+  n = 0;
+}
 
 static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenConst &C, ScenState &SS, InstState &x,
-                            long long lb, long long t_end, int2 *stage) {
+                                   long long lb, long long t_end, AdvStage &sm) {
   const unsigned lane = lane_id();
   const int cap = C.cap;
   const long long k5 = P.k5;
-  int rem[kR], rid[kR];
+  int rem[kR], rid[kR], tq[kR], fin[kR];     // remaining, id, target T, final context p + T
   unsigned live[kR];
 #pragma unroll
   for (int q = 0; q < kR; ++q) {
     const int s = q * 32 + (int)lane;
-    rem[q] = kDead; rid[q] = 0;
+    rem[q] = kDead; rid[q] = 0; tq[q] = 0; fin[q] = 0;
     if (s < x.run_n) { rem[q] = D.run_rem[lb + s]; rid[q] = D.run_id[lb + s]; }
     live[q] = __ballot_sync(0xffffffffu, s < x.run_n);
   }
-  int nlive = x.run_n, tail = x.run_n;
+#pragma unroll
+  for (int q = 0; q < kR; ++q)
+    if ((live[q] >> lane) & 1u) {
+      tq[q] = D.T[C.traj_off + rid[q]];
+      fin[q] = D.prompt[C.grp_off + grp_of(P, rid[q])] + tq[q];
+    }
+  // arrivals 0..31 of this window: lane k holds arrival k
+  int a_id = 0, a_gen = 0, a_T = 0, a_p = 0;
+  if ((int)lane < x.arr_n) {
+    a_id = D.arr_id[lb + lane];
+    const long long j = C.traj_off + a_id;
+    a_gen = D.gen[j]; a_T = D.T[j]; a_p = D.prompt[C.grp_off + grp_of(P, a_id)];
+  }
+  int arr_ring0 = -1;                       // wait-ring position of arrival 0 once appended
+  int nlive = x.run_n, tail = x.run_n, n_ev = 0;
   long long next_arr = x.arr_head < x.arr_n ? D.arr_t[lb + x.arr_head] : kInf;
   bool head_ok = false, blocked = false;
   int head_id = 0, head_gen = 0, head_T = 0;
@@ -102,14 +136,27 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
       x.kv += k5 * n0;
       x.tokens += n0;
       if (dany) {
-        long long release = 0;
         int ncomp = 0;
 #pragma unroll
+        for (int q = 0; q < kR; ++q) ncomp += __popc(d[q]);
+        if (n_ev + ncomp > kEvBuf) flush_events(D, C, SS, sm.ev, n_ev);
+        long long release = 0;
+        int before = n_ev;
+#pragma unroll
         for (int q = 0; q < kR; ++q) {
-          if ((d[q] >> lane) & 1u) { emit_completion(P, D, C, SS, rid[q], b, release); rem[q] = kDead; }
+          if ((d[q] >> lane) & 1u) {
+            const long long j = C.traj_off + rid[q];
+            release += k5 * (long long)fin[q];
+            D.gen[j] = tq[q];
+            D.loc[j] = L_DONE;
+            D.t_complete[j] = b;                         // reward due at b + R
+            sm.ev[before + __popc(d[q] & lanemask_lt())] = rid[q];
+            rem[q] = kDead;
+          }
+          before += __popc(d[q]);
           live[q] &= ~d[q];
-          ncomp += __popc(d[q]);
         }
+        n_ev = before;
         release = warp_sum(release);
         x.kv -= release;
         nlive -= ncomp;
@@ -121,6 +168,7 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
           if (live[q]) t = q * 32 + 32 - __clz(live[q]);
         tail = t;
         blocked = false;
+        __syncwarp();
       }
       x.st = I_IDLE;
     } else if (pull_done) {
@@ -134,17 +182,18 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
         for (int q = 0; q < kR; ++q)
           if (live[q]) hq = q;
         unsigned hm = 0;
-        int r_ = 0, i_ = 0;
+        int r_ = 0, i_ = 0, t_ = 0, f_ = 0;
 #pragma unroll
         for (int q = 0; q < kR; ++q)
-          if (q == hq) { hm = live[q]; r_ = rem[q]; i_ = rid[q]; }
+          if (q == hq) { hm = live[q]; r_ = rem[q]; i_ = rid[q]; t_ = tq[q]; f_ = fin[q]; }
         const int hl = 31 - __clz(hm);
         const int r = __shfl_sync(0xffffffffu, r_, hl);
         const int id = __shfl_sync(0xffffffffu, i_, hl);
+        const int Tj = __shfl_sync(0xffffffffu, t_, hl);
+        const int fj = __shfl_sync(0xffffffffu, f_, hl);
         const long long j = C.traj_off + id;
-        const int Tj = D.T[j];
         const int g_ = Tj - r;
-        const long long ctx = D.prompt[C.grp_off + id / P.G] + g_;
+        const long long ctx = fj - r;                  // p + gen
         x.kv -= k5 * ctx;
         x.whead = x.whead == 0 ? cap - 1 : x.whead - 1;
         if (lane == 0) {
@@ -181,6 +230,7 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
         const int id = D.arr_id[lb + x.arr_head];
         int pos = x.whead + x.wn;
         if (pos >= cap) pos -= cap;
+        if (x.arr_head == 0) arr_ring0 = pos;
         if (lane == 0) { D.wait_id[lb + pos] = id; D.loc[C.traj_off + id] = L_WAIT; }
         ++x.wn;
         ++x.arr_head;
@@ -192,11 +242,25 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
     if (x.wn > 0 && !blocked) {
       while (x.wn > 0) {
         if (!head_ok) {
-          head_id = D.wait_id[lb + x.whead];
-          const long long j = C.traj_off + head_id;
-          head_gen = D.gen[j];
-          head_T = D.T[j];
-          head_ctx = D.prompt[C.grp_off + head_id / P.G] + head_gen;
+          // the head is arrival k of this window when its ring position is arr_ring0 + k
+          int k = -1;
+          if (arr_ring0 >= 0) {
+            k = x.whead - arr_ring0;
+            if (k < 0) k += cap;
+            if (k >= x.arr_head || k >= 32) k = -1;
+          }
+          if (k >= 0) {
+            head_id = __shfl_sync(0xffffffffu, a_id, k);
+            head_gen = __shfl_sync(0xffffffffu, a_gen, k);
+            head_T = __shfl_sync(0xffffffffu, a_T, k);
+            head_ctx = __shfl_sync(0xffffffffu, a_p, k) + head_gen;
+          } else {
+            head_id = D.wait_id[lb + x.whead];
+            const long long j = C.traj_off + head_id;
+            head_gen = D.gen[j];
+            head_T = D.T[j];
+            head_ctx = D.prompt[C.grp_off + grp_of(P, head_id)] + head_gen;
+          }
           head_ok = true;
         }
         if (x.kv + k5 * head_ctx > P.M) { blocked = true; break; }
@@ -208,14 +272,15 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
 #pragma unroll
             for (int qq = 0; qq < kR; ++qq)
               if (qq < q) before += __popc(live[qq]);
-            if ((live[q] >> lane) & 1u) stage[before + __popc(live[q] & lanemask_lt())] = make_int2(rem[q], rid[q]);
+            if ((live[q] >> lane) & 1u)
+              sm.compact[before + __popc(live[q] & lanemask_lt())] = make_int4(rem[q], rid[q], tq[q], fin[q]);
           }
           __syncwarp();
 #pragma unroll
           for (int q = 0; q < kR; ++q) {
             const int s = q * 32 + (int)lane;
             rem[q] = kDead;
-            if (s < nlive) { const int2 e = stage[s]; rem[q] = e.x; rid[q] = e.y; }
+            if (s < nlive) { const int4 e = sm.compact[s]; rem[q] = e.x; rid[q] = e.y; tq[q] = e.z; fin[q] = e.w; }
             live[q] = __ballot_sync(0xffffffffu, s < nlive);
           }
           __syncwarp();
@@ -226,7 +291,10 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
 #pragma unroll
         for (int q = 0; q < kR; ++q)
           if (q == sq) {
-            if ((int)lane == sl) { rem[q] = head_T - head_gen; rid[q] = head_id; }
+            if ((int)lane == sl) {
+              rem[q] = head_T - head_gen; rid[q] = head_id;
+              tq[q] = head_T; fin[q] = (int)(head_ctx - head_gen) + head_T;
+            }
             live[q] |= 1u << sl;
           }
         if (lane == 0) D.loc[C.traj_off + head_id] = L_RUN;
@@ -273,6 +341,7 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
       }
     }
   }
+  flush_events(D, C, SS, sm.ev, n_ev);
   // write the run list back compacted, in admission order
   int before = 0;
 #pragma unroll
@@ -342,7 +411,7 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
       const int id = D.run_id[lb + k];
       const long long j = C.traj_off + id;
       const int g_ = D.T[j] - D.run_rem[lb + k];
-      x.kv -= k5 * (long long)(D.prompt[C.grp_off + id / P.G] + g_);
+      x.kv -= k5 * (long long)(D.prompt[C.grp_off + grp_of(P, id)] + g_);
       x.whead = x.whead == 0 ? cap - 1 : x.whead - 1;
       if (lane == 0) {
         D.gen[j] = g_;
@@ -374,7 +443,7 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
       const int id = D.wait_id[lb + x.whead];
       const long long j = C.traj_off + id;
       const int gj = D.gen[j];
-      const long long ctx = D.prompt[C.grp_off + id / P.G] + gj;
+      const long long ctx = D.prompt[C.grp_off + grp_of(P, id)] + gj;
       if (x.kv + k5 * ctx > P.M) break;
       if (lane == 0) {
         D.run_id[lb + x.run_n] = id;
@@ -401,7 +470,7 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
 }
 
 // One window of W6-W7 for global instance gi, executed by one warp (stage: 32*kR int2 of smem).
-__device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D, int gi, int2 *stage) {
+__device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D, int gi, AdvStage &stage) {
   const unsigned lane = lane_id();
   const int s = D.inst_scen[gi];
   const ScenConst C = D.sc[s];

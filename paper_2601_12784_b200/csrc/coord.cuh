@@ -61,6 +61,18 @@ __device__ __forceinline__ bool verify_free(const int *sfree, int v, int cu, int
   return false;
 }
 
+// verify(v) for every v = cu - eta + d, d in [0, eta], as a bitmask: bit d is set iff one of
+// the buffers cu .. cu + d has a free slot (the reserve range [max(v, cu), v + eta] = [cu, cu+d]).
+// Versions below cu - eta can never verify.
+__device__ __forceinline__ unsigned verify_mask(const int *sfree, int eta) {
+  unsigned m = 0, any = 0;
+  for (int d = 0; d <= eta; ++d) {
+    any |= sfree[d] > 0;
+    m |= any << d;
+  }
+  return m;
+}
+
 __device__ __forceinline__ void log_cmd(const GParams &P, const Dev &D, const ScenConst &C, Cyc &c, int kind,
                                         int inst, int traj) {
   c.hash = fnv_words(c.hash, c.window, kind, inst, traj);
@@ -76,7 +88,7 @@ __device__ __forceinline__ void log_cmd(const GParams &P, const Dev &D, const Sc
 // into D.mlq[mlq_off ...].  Versions lie in [max(0, cu - eta), ps]; items are bucketed stably by
 // version with packed (v - vlo) << 27 | id keys.  Returns the count; *min_v = smallest version
 // present (INT_MAX if none, -1 if an item's version is out of range: protocol bug).
-static __device__ int build_mlq(const Dev &D, const ScenConst &C, const Cyc &c, Stage &sg, int *min_v) {
+static __device__ int build_mlq(const GParams &P, const Dev &D, const ScenConst &C, const Cyc &c, Stage &sg, int *min_v) {
   const unsigned lane = lane_id();
   const int w_lo = (c.min_live_g * c.G) >> 5;
   const int w_hi = (c.n_ingested * c.G + 31) >> 5;
@@ -108,7 +120,7 @@ static __device__ int build_mlq(const Dev &D, const ScenConst &C, const Cyc &c, 
     const int k = k0 + (int)lane;
     if (k < n_tmp) {
       const int id = tmp[k];
-      const int d = D.gv[C.grp_off + id / c.G] - vlo;
+      const int d = D.gv[C.grp_off + grp_of(P, id)] - vlo;
       if (d < 0 || d >= nv) bad = true;
       else { tmp[k] = (d << 27) | id; atomicAdd(&sg.vcnt[d], 1); }
     }
@@ -151,6 +163,8 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
   const unsigned lane = lane_id();
   const int total = c.n_v + c.n_vl;
   int pass_group = -1, pass_vg = -1, routed = 0;
+  unsigned vmask = verify_mask(sfree, c.eta);
+  const int vbase = c.cu - c.eta;
   double Tcur[KS];                                   // Eq 2 of each owned instance's current S
 #pragma unroll
   for (int q = 0; q < KS; ++q) Tcur[q] = throughput_d(P, S.n[q], S.kv[q]);
@@ -164,7 +178,7 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
       const int kk = k0 + (int)lane;
       if (kk < total) {
         p_id = kk < c.n_v ? D.mlq[C.mlq_off + kk] : c.vl_head * c.G + (kk - c.n_v);
-        const int g = p_id / c.G;
+        const int g = grp_of(P, p_id);
         p_vg = D.gv[C.grp_off + g];
         p_l = D.prompt[C.grp_off + g] + D.gen[C.traj_off + p_id];
         if (tentative < 0) p_ready = D.ready[C.traj_off + p_id];
@@ -174,7 +188,7 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
     for (int a = 0; a < nb; ++a) {
       k = k0 + a;
       const int id = __shfl_sync(0xffffffffu, p_id, a);
-      const int g = id / c.G;
+      const int g = grp_of(P, id);
       int vg = __shfl_sync(0xffffffffu, p_vg, a);
       if (vg < 0 && g == pass_group) vg = pass_vg;
       const int l = __shfl_sync(0xffffffffu, p_l, a);
@@ -184,7 +198,7 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
 #pragma unroll
       for (int q = 0; q < KS; ++q) {
         const int i = (int)lane + 32 * q;
-        cand[q] = i < c.I && (vg < 0 ? verify_free(sfree, S.v[q], c.cu, c.eta) : S.v[q] >= vg);
+        cand[q] = i < c.I && (vg < 0 ? (S.v[q] >= vbase && ((vmask >> (S.v[q] - vbase)) & 1u)) : S.v[q] >= vg);
         any |= cand[q];
       }
       if (!__any_sync(0xffffffffu, any)) { stop = true; break; }
@@ -255,6 +269,7 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
         __syncwarp();
         if (lane == 0) sfree[b - c.cu] -= 1;
         __syncwarp();
+        vmask = verify_mask(sfree, c.eta);
         if (tentative < 0) {
           // latest empty slot = highest index in ring buffer b
           const int ring = b % (c.eta + 1);
@@ -348,7 +363,7 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
     c.vl_head = c.n_ingested;
   } else if (k >= c.n_v) {
     const int id = c.vl_head * c.G + (k - c.n_v);
-    const int g = id / c.G;
+    const int g = grp_of(P, id);
     if (g == pass_group) {
       // group versioned in this pass but only partly routed: its other members join the
       // versioned part of the TS
@@ -586,7 +601,7 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
     __syncwarp();
     const bool vanilla_route = !(C.strategy & 1), vanilla_sync = !(C.strategy & 2), sf_mig = (C.strategy & 4) != 0;
     int min_v = 0x7fffffff;
-    c.n_v = build_mlq(D, C, c, sg, &min_v);
+    c.n_v = build_mlq(P, D, C, c, sg, &min_v);
     if (min_v < 0) c.mlq_err = 1;
     c.n_vl = (c.n_ingested - c.vl_head) * c.G;
 
@@ -719,7 +734,7 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
       }
     }
     // ---------------- W5: routing (Alg 2) over the TS incl. interrupted trajectories
-    c.n_v = build_mlq(D, C, c, sg, &min_v);
+    c.n_v = build_mlq(P, D, C, c, sg, &min_v);
     if (min_v < 0) c.mlq_err = 1;
     const int nr = route_pass<KS>(P, D, C, c, S, sfree, acc_delta, arrn, sg, vanilla_route, -1);
     m_routes = nr;

@@ -5,7 +5,7 @@
 namespace sf {
 
 __global__ void __launch_bounds__(32 * kWarpsPerBlock) k_advance(GParams P, Dev D, int n_inst_total) {
-  __shared__ int2 stage_all[kWarpsPerBlock][32 * kR];
+  __shared__ AdvStage stage_all[kWarpsPerBlock];
   const int gi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (gi >= n_inst_total) return;
   advance_instance(P, D, gi, stage_all[threadIdx.x >> 5]);

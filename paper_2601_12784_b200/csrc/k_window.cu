@@ -17,7 +17,7 @@ constexpr int kFusedWarps = 4;
 
 union WinStage {
   Stage coord;
-  int2 adv[32 * kR];
+  AdvStage adv;
   EvStage led;
 };
 

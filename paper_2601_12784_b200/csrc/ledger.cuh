@@ -141,7 +141,7 @@ __device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, 
       const int e = valid ? es.srt[k] : 0;
       const int id = es.id[e];
       const bool ok = valid && es.t[e] + P.R <= t_end;
-      const int g = id / P.G;
+      const int g = grp_of(P, id);
       const unsigned okm = __ballot_sync(0xffffffffu, ok);
       const int nrw = ok ? D.n_rew[C.grp_off + g] : 0;
       const unsigned same = __match_any_sync(0xffffffffu, ok ? g : -1 - (int)lane);
@@ -177,7 +177,7 @@ __device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, 
     for (; np < n; ++np) {
       const int id = tmp[np];
       if (D.t_complete[C.traj_off + id] + P.R > t_end) break;
-      const int g = id / P.G;
+      const int g = grp_of(P, id);
       const int nr = D.n_rew[C.grp_off + g] + 1;
       __syncwarp();
       if (lane == 0) D.n_rew[C.grp_off + g] = nr;

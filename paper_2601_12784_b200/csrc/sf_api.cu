@@ -138,7 +138,7 @@ void prof_mark(sf_ctx *c, int kind) {
 extern "C" {
 
 sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf_config *cfg, sf_ctx **out) {
-  if (!cfg || !out || group_size < 1 || cfg->batch_size < 1 || cfg->n_scenarios < 1 || cfg->k5_tok < 1 ||
+  if (!cfg || !out || group_size < 1 || group_size > 4096 || cfg->batch_size < 1 || cfg->n_scenarios < 1 || cfg->k5_tok < 1 ||
       cfg->snap_period_ps <= 0 || cfg->pool_capacity_groups < 1 || cfg->kv_budget_tok < 1 ||
       cfg->command_log_capacity < 0 || cfg->route_lat_ps < 0 || cfg->pull_lat_ps < 0 || cfg->reward_lat_ps < 0 ||
       cfg->auto_train_windows < 0)
@@ -159,6 +159,7 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
   P.k1 = cfg->k1_ps_per_tok; P.k2 = cfg->k2_ps; P.k3 = cfg->k3_ps; P.k4 = cfg->k4_ps;
   P.k5 = cfg->k5_tok; P.kp = cfg->kprefill_ps_per_tok; P.M = cfg->kv_budget_tok;
   P.k1i = (int)P.k1; P.k3i = (int)P.k3; P.kpi = (int)P.kp;
+  P.gmag = ((1ULL << 40) + G - 1) / G;           // grp_of() multiply-shift (sf_internal.cuh)
   P.mu = cfg->mu; P.phi_tp = cfg->phi_throughput; P.phi_wait = cfg->phi_wait;
   P.delta = cfg->snap_period_ps; P.r = cfg->route_lat_ps; P.q = cfg->pull_lat_ps; P.R = cfg->reward_lat_ps;
   P.atw = cfg->auto_train_windows; P.pool_cap = cfg->pool_capacity_groups;

@@ -74,3 +74,13 @@ def test_oracle_is_independent_of_the_product():
                 src = open(os.path.join(dp, f)).read()
                 for b in bad_in_product:
                     assert b not in src, f"{f} references {b}"
+
+
+def test_group_division_multiply_shift_exact():
+    """grp_of() (sf_internal.cuh): id / G == (id * ceil(2^40/G)) >> 40 for id < 2^27, G <= 4096."""
+    import random
+    rng = random.Random(7)
+    for G in list(range(1, 65)) + [96, 100, 1000, 4095, 4096]:
+        m = ((1 << 40) + G - 1) // G
+        ids = list(range(5000)) + [rng.randrange(1 << 27) for _ in range(5000)] + [(1 << 27) - 1 - k for k in range(500)]
+        assert all((i * m) >> 40 == i // G for i in ids), G
