@@ -12,6 +12,7 @@
 // takes the highest live slot.  The list is written back compacted at the window end.
 // Fallback path: the same procedure streaming the run list through global memory.
 #pragma once
+#include <cassert>
 #include "sf_internal.cuh"
 
 namespace sf {
@@ -213,6 +214,7 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
         ++x.wn;
         ++x.preempts;
         head_ok = true; head_id = id; head_gen = g_; head_T = Tj; head_ctx = ctx;
+        arr_ring0 = -1;      // the front push may reuse ring slots of admitted arrivals: stop mapping
       }
       blocked = true;                                 // the last victim (the head) cannot re-fit now
     }
@@ -342,6 +344,12 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
     }
   }
   flush_events(D, C, SS, sm.ev, n_ev);
+#ifdef SF_CHECK
+  assert(SS.ev_n <= C.cap);
+  assert(nlive >= 0 && nlive <= 32 * kR && x.wn >= 0 && x.wn <= cap && x.kv >= 0 && x.kv <= P.M);
+#pragma unroll
+  for (int q = 0; q < kR; ++q) assert(!((live[q] >> lane) & 1u) || (rem[q] > 0 && rem[q] <= tq[q]));
+#endif
   // write the run list back compacted, in admission order
   int before = 0;
 #pragma unroll

@@ -7,6 +7,7 @@
 // earlier Reserved entries into the hole, then Occupy the earliest empty slot
 // (P:366).  Slot searches are warp ballots over 32 slots at a time.
 #pragma once
+#include <cassert>
 #include "sf_internal.cuh"
 
 namespace sf {
@@ -113,6 +114,9 @@ __device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, 
   if (SS.err) return;
   const long long t_end = SS.t + P.delta;
   const int n = SS.ev_n;
+#ifdef SF_CHECK
+  assert(n >= 0 && n <= C.cap);
+#endif
   const int cu = SS.cu;
   int err = 0;
   long long m_reloc = 0, m_occ = 0;

@@ -113,14 +113,33 @@ def test_c5_full_size_sampled(launch_mode):
     n = len(p.scenarios)
     prs, tgs = zip(*[W.draw_lengths(p, k, p.pool_groups) for k in range(n)])
     assert g.submit_many(np.arange(n), np.full(n, p.pool_groups), np.concatenate(prs), np.concatenate(tgs)) == 0
-    g.step(60)
+    g.step(130)
     sample = sorted(random.Random(2026).sample(range(n), 48))
     o = OracleSim.from_preset(p, sample)
     for a, k in enumerate(sample):
         assert o.submit(a, prs[k], tgs[k]) == 0
-    assert o.step(60, 8) == 0
+    assert o.step(130, 8) == 0
     for a, k in enumerate(sample):
         mo, mg = o.metrics(a), g.metrics(k)
         assert (mo == mg).all(), f"scenario {k}: {np.nonzero(mo != mg)}"
         assert (o.lifecycles(a) == g.lifecycles(k)).all()
         assert (o.batches(a) == g.batches(k)).all()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_preemption_stress(seed, launch_mode):
+    """Tight KV budget and many arrivals per instance: preemptions interleaved with arrival
+    admissions inside one window (the register arrival-prefetch path of k_advance)."""
+    rng = random.Random(900 + seed)
+    I, eta, G, B = rng.randint(1, 2), rng.randint(0, 2), 4, 16
+    cfg = Config(batch_size=B, n_scenarios=1, k1=1, k2=100, k3=10, k4=50, k5=1, kp=1, M=1500, mu=0.05,
+                 phi_tp=50.0, phi_wait=1000, delta=30000, r=5, q=3000, R=5000, strategy=rng.choice([7, 6, 3]),
+                 atw=2, pool_capacity_groups=B * 5)
+    steps = 4
+    prompt = np.array([rng.randint(1, 120) for _ in range(B * steps)], np.int32)
+    target = np.array([rng.randint(1, 300) for _ in range(B * steps * G)], np.int32)
+    o = OracleSim(I, eta, G, cfg)
+    g = gpu_from_config(I, eta, G, cfg)
+    assert o.submit(0, prompt, target) == 0 and g.submit(0, prompt, target) == 0
+    run_lockstep(o, g, [0], 150, every=3)
+    assert o.metrics()[8] > 0                  # preemptions happened
