@@ -235,7 +235,7 @@ def main():
     local_iters = int(m1[2] - m0[2])
     dm = torch.tensor((m1 - m0).astype(np.int64), device="cuda")
     tm = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    adv = torch.tensor([kern_ms[1]], dtype=torch.float64, device="cuda")
+    adv = torch.tensor([kern_ms.max()], dtype=torch.float64, device="cuda")
     reduce_metrics(dm, world, dist)                     # the metrics all-reduce (NCCL over NVLink)
     if world > 1:
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
@@ -246,8 +246,10 @@ def main():
 
     # ---------------- roofline of the dominant kernel (k_advance) from the live CUDA events
     hbm, peak_src, _ = peaks()
-    adv_ms_per_launch = kern_ms[1] / max(1, kern_n[1])
-    bytes_per_launch = ALGO_BYTES_PER_ITER * local_iters / max(1, kern_n[1])
+    kid = int(np.argmax(kern_ms))                       # dominant kernel of the step
+    kname = ("k_begin_coord", "k_advance", "k_ledger", "k_window")[kid]
+    adv_ms_per_launch = kern_ms[kid] / max(1, kern_n[kid])
+    bytes_per_launch = ALGO_BYTES_PER_ITER * local_iters / max(1, kern_n[kid])
     achieved = bytes_per_launch / (adv_ms_per_launch / 1e3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_advance_traffic.json")
@@ -256,7 +258,8 @@ def main():
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    share = {k: kern_ms[i] / max(1e-9, kern_ms[:3].sum()) for i, k in enumerate(("coordinate", "advance", "ledger"))}
+    share = {k: kern_ms[i] / max(1e-9, kern_ms.sum())
+             for i, k in enumerate(("coordinate", "advance", "ledger", "fused_window")) if kern_n[i]}
 
     # ---------------- e2e: the same metric through the C ABI with host buffers
     e2e = None
@@ -277,10 +280,10 @@ def main():
                        "scenarios_per_gpu": S, "global_scenarios": S * world, "windows_per_step": 1,
                        "parallelism": f"scenario-sharded x{world}", "l2": f"flushed ({args.flush_mb} MiB write) "
                                                                           "between timed windows"},
-            "roofline": {"bound": "hbm", "kernel": "k_advance", "achieved": achieved, "peak": hbm,
+            "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm,
                          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                          "algorithmic_bytes_per_traj_iter": ALGO_BYTES_PER_ITER,
-                         "launches": int(kern_n[1]), "ms_per_launch": adv_ms_per_launch,
+                         "launches": int(kern_n[kid]), "ms_per_launch": adv_ms_per_launch,
                          "step_share": share},
             "cpu_baseline": cpu,
             "e2e": e2e,

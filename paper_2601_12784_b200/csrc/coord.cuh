@@ -165,6 +165,8 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
   int pass_group = -1, pass_vg = -1, routed = 0;
   unsigned vmask = verify_mask(sfree, c.eta);
   const int vbase = c.cu - c.eta;
+  int ideal_l = -1;                                  // Eq 4 depends on l only: reuse across group members
+  double thr_l = 0.0;
   double Tcur[KS];                                   // Eq 2 of each owned instance's current S
 #pragma unroll
   for (int q = 0; q < KS; ++q) Tcur[q] = throughput_d(P, S.n[q], S.kv[q]);
@@ -219,8 +221,8 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
         // Steps 2-4: waterfall over version groups.  One reduction on the
         // key (lowest version, highest dT, lowest id) yields the best instance of the lowest
         // remaining version group; accept it if it clears mu * ideal, else retry above that version.
-        const double ideal = ideal_gain_d(P, l);
-        const double thr = __dmul_rn(P.mu, ideal);
+        if (l != ideal_l) { ideal_l = l; thr_l = __dmul_rn(P.mu, ideal_gain_d(P, l)); }
+        const double thr = thr_l;
         double dT[KS];
 #pragma unroll
         for (int q = 0; q < KS; ++q) {
