@@ -81,9 +81,20 @@ bool dalloc(sf_ctx *c, T **p, long long count, int fill_byte) {
 sf_status check_ctx(sf_ctx *c) {
   if (!c) return SF_E_INVALID;
   if (c->poisoned) return SF_E_STATE;
-  cudaSetDevice(c->device);
   return SF_OK;
 }
+
+// Every call runs on the context's device and restores the caller's current device on return.
+struct DevGuard {
+  int prev = -1, dev = -1;
+  explicit DevGuard(int d) : dev(d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DevGuard() {
+    if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+  }
+};
 
 sf_status read_state(sf_ctx *c, int s, ScenState *out) {
   if (!cuda_ok(c, cudaMemcpyAsync(out, c->D.ss + s, sizeof(ScenState), cudaMemcpyDeviceToHost, c->stream), "D2H state") ||
@@ -151,7 +162,10 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
   sf_ctx *c = new (std::nothrow) sf_ctx();
   if (!c) return SF_E_NOMEM;
   c->device = cfg->device;
+  int prev_dev = 0;
+  cudaGetDevice(&prev_dev);
   if (cudaSetDevice(cfg->device) != cudaSuccess) { delete c; return SF_E_CUDA; }
+  struct Restore { int d; ~Restore() { cudaSetDevice(d); } } restore{prev_dev};
   c->stream = (cudaStream_t)cfg->cuda_stream;
   const int ns = cfg->n_scenarios, B = cfg->batch_size, G = group_size;
   GParams &P = c->P;
@@ -253,7 +267,7 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
 
 void sf_destroy(sf_ctx *c) {
   if (!c) return;
-  cudaSetDevice(c->device);
+  DevGuard dg(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   else cudaDeviceSynchronize();
   for (void *p : c->allocs) cudaFree(p);
@@ -267,6 +281,7 @@ sf_status sf_submit_prompts_many(sf_ctx *c, int32_t n, const int32_t *scen_ids, 
                                  const int32_t *prompt, const int32_t *target) {
   sf_status st = check_ctx(c);
   if (st != SF_OK) return st;
+  DevGuard dg(c->device);
   if (n < 0 || (n > 0 && (!scen_ids || !n_groups || !prompt || !target))) return fail(c, SF_E_INVALID, "null argument");
   const int G = c->P.G;
   std::vector<int> desc;
@@ -317,6 +332,7 @@ sf_status sf_submit_prompts(sf_ctx *c, int32_t scenario, int32_t n_groups, const
 sf_status sf_step(sf_ctx *c, int32_t n_windows, sf_step_stats *out) {
   sf_status st = check_ctx(c);
   if (st != SF_OK) return st;
+  DevGuard dg(c->device);
   if (n_windows < 0) return fail(c, SF_E_INVALID, "n_windows < 0");
   long long before[sf::kMetrics] = {0}, after[sf::kMetrics] = {0};
   if (out && (st = reduce_metrics_host(c, before)) != SF_OK) return st;
@@ -362,6 +378,7 @@ sf_status sf_step(sf_ctx *c, int32_t n_windows, sf_step_stats *out) {
 sf_status sf_publish_params(sf_ctx *c, int32_t scenario, int32_t v) {
   sf_status st = check_ctx(c);
   if (st != SF_OK) return st;
+  DevGuard dg(c->device);
   if (scenario < 0 || scenario >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
   ScenState s;
   if ((st = read_state(c, scenario, &s)) != SF_OK) return st;
@@ -380,6 +397,7 @@ sf_status sf_collect_batch(sf_ctx *c, int32_t scenario, int32_t cap, int32_t *v_
                            int32_t *group_versions, int32_t *n_out) {
   sf_status st = check_ctx(c);
   if (st != SF_OK) return st;
+  DevGuard dg(c->device);
   if (scenario < 0 || scenario >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
   const int B = c->P.B;
   if (n_out) *n_out = B;
@@ -405,6 +423,7 @@ sf_status sf_collect_batch(sf_ctx *c, int32_t scenario, int32_t cap, int32_t *v_
 sf_status sf_read_metrics(sf_ctx *c, int64_t *out, int32_t len) {
   sf_status st = check_ctx(c);
   if (st != SF_OK) return st;
+  DevGuard dg(c->device);
   if (!out || len < 0) return fail(c, SF_E_INVALID, "bad output");
   long long m[sf::kMetrics];
   if ((st = reduce_metrics_host(c, m)) != SF_OK) return st;
@@ -415,6 +434,7 @@ sf_status sf_read_metrics(sf_ctx *c, int64_t *out, int32_t len) {
 sf_status sf_read_metrics_device(sf_ctx *c, int64_t *out_dev) {
   sf_status st = check_ctx(c);
   if (st != SF_OK) return st;
+  DevGuard dg(c->device);
   if (!out_dev) return fail(c, SF_E_INVALID, "null output");
   sf_launch_reduce_metrics(c->D, c->n_scen, (long long *)out_dev, c->stream);
   c->launches++;
@@ -424,6 +444,7 @@ sf_status sf_read_metrics_device(sf_ctx *c, int64_t *out_dev) {
 sf_status sf_read_scenario_metrics(sf_ctx *c, int32_t scenario, int64_t *out, int32_t len) {
   sf_status st = check_ctx(c);
   if (st != SF_OK) return st;
+  DevGuard dg(c->device);
   if (scenario < 0 || scenario >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
   ScenState s;
   if ((st = read_state(c, scenario, &s)) != SF_OK) return st;
@@ -449,6 +470,7 @@ static sf_status ensure_dump(sf_ctx *c, size_t n) {
 sf_status sf_dump_lifecycles(sf_ctx *c, int32_t scenario, int64_t *rec, int64_t cap, int64_t *n) {
   sf_status st = check_ctx(c);
   if (st != SF_OK) return st;
+  DevGuard dg(c->device);
   if (scenario < 0 || scenario >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
   const long long cnt = (long long)c->hn_pool[scenario] * c->P.G;
   if (n) *n = cnt;
@@ -467,6 +489,7 @@ sf_status sf_dump_lifecycles(sf_ctx *c, int32_t scenario, int64_t *rec, int64_t 
 sf_status sf_dump_batches(sf_ctx *c, int32_t scenario, int32_t *out, int64_t cap, int64_t *n) {
   sf_status st = check_ctx(c);
   if (st != SF_OK) return st;
+  DevGuard dg(c->device);
   if (scenario < 0 || scenario >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
   ScenState s;
   if ((st = read_state(c, scenario, &s)) != SF_OK) return st;
@@ -484,6 +507,7 @@ sf_status sf_dump_batches(sf_ctx *c, int32_t scenario, int32_t *out, int64_t cap
 sf_status sf_dump_commands(sf_ctx *c, int32_t scenario, int64_t *rec, int64_t cap, int64_t *n) {
   sf_status st = check_ctx(c);
   if (st != SF_OK) return st;
+  DevGuard dg(c->device);
   if (scenario < 0 || scenario >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
   ScenState s;
   if ((st = read_state(c, scenario, &s)) != SF_OK) return st;
@@ -501,6 +525,7 @@ sf_status sf_dump_commands(sf_ctx *c, int32_t scenario, int64_t *rec, int64_t ca
 sf_status sf_dump_instances(sf_ctx *c, int32_t scenario, int64_t *out, int64_t cap, int64_t *n) {
   sf_status st = check_ctx(c);
   if (st != SF_OK) return st;
+  DevGuard dg(c->device);
   if (scenario < 0 || scenario >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
   const int I = c->hsc[scenario].I;
   if (n) *n = I;
@@ -529,6 +554,7 @@ sf_status sf_debug_coord_cycles(sf_ctx *c, int64_t *out) {
 sf_status sf_profile(sf_ctx *c, int32_t enable) {
   sf_status st = check_ctx(c);
   if (st != SF_OK) return st;
+  DevGuard dg(c->device);
   c->prof_on = enable ? 1 : 0;
   return SF_OK;
 }
@@ -536,6 +562,7 @@ sf_status sf_profile(sf_ctx *c, int32_t enable) {
 sf_status sf_profile_read(sf_ctx *c, double *ms, int64_t *launches, int32_t len) {
   sf_status st = check_ctx(c);
   if (st != SF_OK) return st;
+  DevGuard dg(c->device);
   if (!cuda_ok(c, cudaStreamSynchronize(c->stream), "sync")) return SF_E_CUDA;
   for (size_t k = 0; k + 1 < c->ev_used; k += 2) {
     float e = 0.f;

@@ -111,11 +111,13 @@ class StaleFlow:
                  phi_wait: int = W.PHI_WAIT, snap_period: int = W.PS_PER_S, route_lat: int = 10_000_000_000,
                  pull_lat: int = 2 * W.PS_PER_S, reward_lat: int = W.PS_PER_S, strategy: int = W.STRAT_SF,
                  auto_train_windows: int = 0, pool_capacity_groups: int = 1024, command_log_capacity: int = 0,
-                 device: int = 0, stream=None):
+                 device: Optional[int] = None, stream=None):
         import torch  # device + stream plumbing only
         if not torch.cuda.is_available():
             raise SfError("StaleFlow needs a CUDA device (no CPU fallback)")
         self.L = load_library()
+        if device is None:
+            device = torch.cuda.current_device()
         self.G, self.B, self.n_scen = group_size, batch_size, n_scenarios
         if stream is None:
             stream = torch.cuda.current_stream(device)
