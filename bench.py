@@ -251,11 +251,13 @@ def main():
     adv_ms_per_launch = kern_ms[kid] / max(1, kern_n[kid])
     bytes_per_launch = ALGO_BYTES_PER_ITER * local_iters / max(1, kern_n[kid])
     achieved = bytes_per_launch / (adv_ms_per_launch / 1e3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_advance_traffic.json")
+    traffic = None                                      # ncu dram bytes per launch of that kernel
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+            for k, v in json.load(open(tpath))["dram_bytes_per_launch"].items():
+                if kname in k:
+                    traffic = v
         except Exception:
             traffic = None
     share = {k: kern_ms[i] / max(1e-9, kern_ms.sum())

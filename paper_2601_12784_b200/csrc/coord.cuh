@@ -738,7 +738,13 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
     // ---------------- W5: routing (Alg 2) over the TS incl. interrupted trajectories
     c.n_v = build_mlq(P, D, C, c, sg, &min_v);
     if (min_v < 0) c.mlq_err = 1;
+#ifdef SF_TIMING
+    const long long t_rp = clock64();
+#endif
     const int nr = route_pass<KS>(P, D, C, c, S, sfree, acc_delta, arrn, sg, vanilla_route, -1);
+#ifdef SF_TIMING
+    dbg_tent = (int)(clock64() - t_rp);          // (slot 7) cycles in the real routing pass
+#endif
     m_routes = nr;
     m_reserves = c.reserves;
     // write back per-instance route effects (Table 1 Route row)
