@@ -120,6 +120,9 @@ sf_status sf_read_metrics(sf_ctx *ctx, int64_t *out, int32_t len);
 sf_status sf_read_metrics_device(sf_ctx *ctx, int64_t *out_dev);
 /* One scenario's cumulative metrics (host out[len]). */
 sf_status sf_read_scenario_metrics(sf_ctx *ctx, int32_t scenario, int64_t *out, int32_t len);
+/* Every scenario's cumulative metrics in one transfer: out[n_scenarios * SF_METRICS_LEN]
+ * (host), scenario-major; slots 25/26/29/30 as in sf_read_scenario_metrics. */
+sf_status sf_read_all_scenario_metrics(sf_ctx *ctx, int64_t *out, int64_t cap);
 
 /* Per-trajectory lifecycle records, 13 int64 each: id, group, prompt, target, gen, v_group,
  * state (0 pool,1 TS,2 transit,3 wait,4 run,5 done,6 consumed), inst, n_routes, n_preempt,

@@ -458,6 +458,28 @@ sf_status sf_read_scenario_metrics(sf_ctx *c, int32_t scenario, int64_t *out, in
   return SF_OK;
 }
 
+sf_status sf_read_all_scenario_metrics(sf_ctx *c, int64_t *out, int64_t cap) {
+  sf_status st = check_ctx(c);
+  if (st != SF_OK) return st;
+  DevGuard dg(c->device);
+  if (!out || cap < (int64_t)c->n_scen * sf::kMetrics) return fail(c, SF_E_RANGE, "output too small");
+  std::vector<ScenState> ss(c->n_scen);
+  if (!cuda_ok(c, cudaMemcpyAsync(ss.data(), c->D.ss, sizeof(ScenState) * c->n_scen, cudaMemcpyDeviceToHost, c->stream),
+               "D2H states") ||
+      !cuda_ok(c, cudaStreamSynchronize(c->stream), "sync"))
+    return SF_E_CUDA;
+  for (int s = 0; s < c->n_scen; ++s) {
+    for (int k = 0; k < sf::kMetrics; ++k) {
+      long long v = (long long)ss[s].m[k];
+      if (k == sf::M_CMD_HASH) v = (long long)ss[s].cmd_hash;
+      if (k == sf::M_SIM_TIME || k == sf::M_MAX_T) v = ss[s].t;
+      if (k == sf::M_ERR_SCEN) v = ss[s].err != 0;
+      out[(long long)s * sf::kMetrics + k] = v;
+    }
+  }
+  return SF_OK;
+}
+
 static sf_status ensure_dump(sf_ctx *c, size_t n) {
   if (n <= c->dump_cap) return SF_OK;
   if (c->d_dump) cudaFree(c->d_dump);

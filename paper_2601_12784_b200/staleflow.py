@@ -25,7 +25,7 @@ STATUS = {0: "SF_OK", 1: "SF_NOT_READY", -1: "SF_E_INVALID", -2: "SF_E_VERSION",
 
 EXPORTS = ["sf_create", "sf_destroy", "sf_submit_prompts", "sf_submit_prompts_many", "sf_step",
            "sf_publish_params", "sf_collect_batch", "sf_read_metrics", "sf_read_metrics_device",
-           "sf_read_scenario_metrics", "sf_dump_lifecycles", "sf_dump_batches", "sf_dump_commands",
+           "sf_read_scenario_metrics", "sf_read_all_scenario_metrics", "sf_dump_lifecycles", "sf_dump_batches", "sf_dump_commands",
            "sf_dump_instances", "sf_kernel_launches", "sf_last_error", "sf_profile", "sf_profile_read"]
 
 
@@ -75,6 +75,7 @@ def load_library(path: str = LIB_PATH):
         "sf_read_metrics": (C.c_int, [P, pI64, I32]),
         "sf_read_metrics_device": (C.c_int, [P, C.c_void_p]),
         "sf_read_scenario_metrics": (C.c_int, [P, I32, pI64, I32]),
+        "sf_read_all_scenario_metrics": (C.c_int, [P, pI64, I64]),
         "sf_dump_lifecycles": (C.c_int, [P, I32, pI64, I64, pI64]),
         "sf_dump_batches": (C.c_int, [P, I32, pI32, I64, pI64]),
         "sf_dump_commands": (C.c_int, [P, I32, pI64, I64, pI64]),
@@ -222,6 +223,12 @@ class StaleFlow:
             self._check(self.L.sf_read_metrics(self.h, _p(out, C.c_int64), METRICS_LEN), "sf_read_metrics")
         else:
             self._check(self.L.sf_read_scenario_metrics(self.h, scen, _p(out, C.c_int64), METRICS_LEN), "metrics")
+        return out
+
+    def all_metrics(self) -> np.ndarray:
+        """(n_scenarios, 32) cumulative per-scenario metrics, one transfer."""
+        out = np.zeros((self.n_scen, METRICS_LEN), np.int64)
+        self._check(self.L.sf_read_all_scenario_metrics(self.h, _p(out, C.c_int64), out.size), "all metrics")
         return out
 
     def metrics_device(self, out_ptr: int):
