@@ -43,7 +43,10 @@ struct Cyc {                   // lane-uniform per-cycle scalars
 
 constexpr int kEmptyWords = 160;   // ledger empty-slot bitmap held in smem when (eta+1)*B <= 5120
 
+constexpr int kGMax = 16;       // group-batched routing for G <= kGMax (route_group_batch)
+
 struct Stage {                 // per-warp shared-memory staging
+  double tab[kGMax][32];       // route_group_batch: Eq 3 gain of lane's instance after j more routes
   unsigned empty[kEmptyWords]; // bit s of ring r: slot s of ring buffer r is Empty (valid if use_bits)
   int sfree[kMaxEta + 1];
   int sfree_tmp[kMaxEta + 1];
@@ -153,6 +156,94 @@ static __device__ int build_mlq(const GParams &P, const Dev &D, const ScenConst 
   return n_tmp;
 }
 
+
+// Group-batched routing (one instance per lane, KS == 1).  After the first member of a
+// versionless group is routed (which fixed v_g and Reserved), its remaining members are the next
+// MLQ items (consecutive ids, same l = p since gen = 0, same candidate set {i : S[i].v >= v_g},
+// same threshold).  Each decision changes only the chosen instance's state, so every lane
+// precomputes its instance's Eq 3 gain after j = 0..nrem-1 further routes of this group (the
+// same operation trees as the one-at-a-time pass: dT = T(n+1, kv+k5 l) - T(n, kv), 0 once
+// gamma fails), and the nrem decisions become reductions over those tables -- no divisions on
+// the sequential chain.  Returns the members routed; *stopped if a member found no instance.
+static __device__ int route_group_batch(const GParams &P, const Dev &D, const ScenConst &C, Cyc &c, InstRegs<1> &S,
+                                 double &Tcur, int &acc_delta, int &arrn, Stage &sg, int id0, int vg, int l,
+                                 int nrem, double thr, int tentative, int &routed, bool &hit, bool &stopped) {
+  const unsigned lane = lane_id();
+  const bool cnd = (int)lane < c.I && S.v[0] >= vg;
+  const long long k5l = (long long)P.k5 * l;
+  {
+    long long kv = S.kv[0];
+    int n = S.n[0];
+    double Tj = Tcur;
+    bool gam = S.w[0] == 0;
+    for (int j = 0; j < nrem; ++j) {
+      double d = 0.0;
+      if (cnd && gam && kv + k5l <= P.M) {
+        const double Tn = throughput_d(P, n + 1, kv + k5l);
+        d = __dsub_rn(Tn, Tj);
+        Tj = Tn; n += 1; kv += k5l;
+      } else {
+        gam = false;
+      }
+      sg.tab[j][lane] = d;
+    }
+  }
+  __syncwarp();
+  int jr = 0, done = 0;
+  for (; done < nrem; ++done) {
+    const double my = cnd ? sg.tab[jr][lane] : 0.0;
+    int sel = -1, last_ver = -1;
+    for (;;) {
+      int bv = 0x7fffffff, bi = 0x7fffffff;
+      double bd = 0.0;
+      if (cnd && S.v[0] > last_ver) { bv = S.v[0]; bd = my; bi = (int)lane; }
+      for (int o = 1; o < c.red_w; o <<= 1) {
+        const int ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov < bv || (ov == bv && (od > bd || (od == bd && oi < bi)))) { bv = ov; bd = od; bi = oi; }
+      }
+      bv = __shfl_sync(0xffffffffu, bv, 0);
+      bd = __shfl_sync(0xffffffffu, bd, 0);
+      bi = __shfl_sync(0xffffffffu, bi, 0);
+      if (bv == 0x7fffffff) break;                     // withhold
+      if (bd >= thr) { sel = bi; break; }              // accept (A4)
+      last_ver = bv;
+    }
+    if (sel < 0) { stopped = true; break; }
+    if (tentative >= 0 && sel == tentative) { hit = true; return done + 1; }
+    const int id = id0 + 1 + done;
+    const int aslot = __shfl_sync(0xffffffffu, arrn, sel);
+    if ((int)lane == sel) { ++jr; ++arrn; ++acc_delta; }
+    if (tentative < 0) {
+      if (lane == 0) {
+        // versionless: never interrupted, so t_ready = t (A18)
+        const long long j = C.traj_off + id;
+        D.loc[j] = L_TRANSIT;
+        D.tinst[j] = (short)sel;
+        atomicAdd(&D.n_routes[j], 1);
+        D.arr_id[C.list_off + (long long)sel * C.cap + aslot] = id;
+        D.arr_t[C.list_off + (long long)sel * C.cap + aslot] = c.t + P.r;
+        if (routed < kArrStage) {
+          sg.arr_t[routed] = c.t + P.r;
+          sg.arr_id[routed] = id;
+          sg.arr_inst[routed] = (short)sel;
+        }
+      }
+      log_cmd(P, D, C, c, CMD_ROUTE, sel, id);
+      ++routed;
+    }
+  }
+  // the snapshot after jr routes to this lane's instance (Eq 3's S')
+  for (int j = 0; j < jr; ++j) {
+    if (S.w[0] == 0 && S.kv[0] + k5l <= P.M) { S.n[0] += 1; S.kv[0] += k5l; }
+    else S.w[0] += 1;
+  }
+  if (jr) Tcur = throughput_d(P, S.n[0], S.kv[0]);
+  __syncwarp();
+  return done;
+}
+
 // One routing pass (Alg 2, or vanilla §6.5) over the MLQ = [versioned n_v items] ++
 // [versionless groups vl_head..n_ingested).  tentative >= 0: Alg 3 trial for that instance on
 // scratch state, returns 1 as soon as a route targets it (early exit allowed).
@@ -172,7 +263,9 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
   for (int q = 0; q < KS; ++q) Tcur[q] = throughput_d(P, S.n[q], S.kv[q]);
   int k = 0;
   bool stop = false;
-  for (int k0 = 0; k0 < total && !stop; k0 += 32) {
+  int knext = 0;
+  while (knext < total && !stop) {
+    const int k0 = knext;
     // prefetch 32 MLQ items: lane a holds item k0 + a
     int p_id = 0, p_vg = -1, p_l = 0;
     long long p_ready = 0;
@@ -187,12 +280,14 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
       }
     }
     const int nb = min(32, total - k0);
-    for (int a = 0; a < nb; ++a) {
+    int a = 0;
+    for (; a < nb; ++a) {
       k = k0 + a;
       const int id = __shfl_sync(0xffffffffu, p_id, a);
       const int g = grp_of(P, id);
       int vg = __shfl_sync(0xffffffffu, p_vg, a);
       if (vg < 0 && g == pass_group) vg = pass_vg;
+      const bool first_member = vg < 0;
       const int l = __shfl_sync(0xffffffffu, p_l, a);
       // Step 1: candidates (check_routable)
       bool cand[KS];
@@ -323,10 +418,8 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
             else S.w[q] += 1;
           }
       }
-      if (tentative >= 0) {
-        if (sel == tentative) return 1;
-        continue;
-      }
+      if (tentative >= 0 && sel == tentative) return 1;
+      if (tentative < 0) {
       // issue Route(sel, id): t_arr = t_ready + r (A18)
       int aslot = 0;
 #pragma unroll
@@ -346,6 +439,7 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
         D.tinst[j] = (short)sel;
         atomicAdd(&D.n_routes[j], 1);
         D.arr_id[C.list_off + (long long)sel * C.cap + aslot] = id;
+        D.arr_t[C.list_off + (long long)sel * C.cap + aslot] = t_arr;
         if (routed < kArrStage) {
           sg.arr_t[routed] = t_arr;
           sg.arr_id[routed] = id;
@@ -355,8 +449,23 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
       }
       log_cmd(P, D, C, c, CMD_ROUTE, sel, id);
       ++routed;
-      if (a == nb - 1) k = k0 + nb;        // pass ran through this batch
+      }
+      // the rest of a versionless group (waterfall only), decided from precomputed gains
+      if constexpr (KS == 1) {
+        if (first_member && !vanilla && c.G > 1 && c.G <= kGMax && k >= c.n_v) {
+          const int nrem = min(c.G - 1, total - (k + 1));
+          if (nrem > 0) {
+            bool hit = false, stopped = false;
+            const int r = route_group_batch(P, D, C, c, S, Tcur[0], acc_delta[0], arrn[0], sg, id, vg, l, nrem,
+                                            thr_l, tentative, routed, hit, stopped);
+            if (hit) return 1;
+            a += r;
+            if (stopped) { k = k0 + a + 1; stop = true; break; }
+          }
+        }
+      }
     }
+    knext = k0 + a;
   }
   if (tentative >= 0) return 0;
   if (!stop) k = total;
@@ -440,25 +549,34 @@ static __device__ void order_arrivals_all(const GParams &P, const Dev &D, const 
 }
 
 static __device__ void order_arrivals_global(const GParams &P, const Dev &D, const ScenConst &C, const Cyc &c, int i, int n) {
+  // t_arr was stored with each route; rank every arrival against 32-wide coalesced chunks of the
+  // list broadcast by shuffles, scatter (id, t) to the scratch, copy back in order.
   const unsigned lane = lane_id();
   const long long lb = C.list_off + (long long)i * C.cap;
-  int *tmp = D.mlq + C.mlq_off;
-  for (int e = lane; e < n; e += 32) {
-    const int ie = D.arr_id[lb + e];
-    const long long te = max(c.t, D.ready[C.traj_off + ie]);
+  int *tid = D.mlq + C.mlq_off;                                  // [0, cap): ids
+  long long *tt = (long long *)(D.mlq + ((C.mlq_off + C.cap + 1) & ~1LL));   // times, 8-byte aligned (3 cap + 2)
+  for (int e0 = 0; e0 < n; e0 += 32) {
+    const int e = e0 + (int)lane;
+    const long long te = e < n ? D.arr_t[lb + e] : 0;
+    const int ie = e < n ? D.arr_id[lb + e] : 0;
     int rank = 0;
-    for (int f = 0; f < n; ++f) {
-      const int jf = D.arr_id[lb + f];
-      const long long tf = max(c.t, D.ready[C.traj_off + jf]);
-      rank += (tf < te) || (tf == te && jf < ie);
+    for (int f0 = 0; f0 < n; f0 += 32) {
+      const int f = f0 + (int)lane;
+      const long long tf = f < n ? D.arr_t[lb + f] : 0x7fffffffffffffffLL;
+      const int jf = f < n ? D.arr_id[lb + f] : 0x7fffffff;
+      const int nb = min(32, n - f0);
+      for (int b = 0; b < nb; ++b) {
+        const long long tb = __shfl_sync(0xffffffffu, tf, b);
+        const int jb = __shfl_sync(0xffffffffu, jf, b);
+        rank += (tb < te) || (tb == te && jb < ie);
+      }
     }
-    tmp[rank] = ie;
+    if (e < n) { tid[rank] = ie; tt[rank] = te; }
   }
   __syncwarp();
   for (int e = lane; e < n; e += 32) {
-    const int ie = tmp[e];
-    D.arr_id[lb + e] = ie;
-    D.arr_t[lb + e] = max(c.t, D.ready[C.traj_off + ie]) + P.r;
+    D.arr_id[lb + e] = tid[e];
+    D.arr_t[lb + e] = tt[e];
   }
   __syncwarp();
 }
@@ -474,6 +592,10 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
   int *sfree = sg.sfree;
 #ifdef SF_TIMING
   const long long t0_clk = clock64();
+  long long ck[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define SF_CK(k) ck[k] = clock64() - t0_clk
+#else
+#define SF_CK(k)
 #endif
 
   Cyc c;
@@ -607,6 +729,7 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
     if (min_v < 0) c.mlq_err = 1;
     c.n_vl = (c.n_ingested - c.vl_head) * c.G;
 
+    SF_CK(0);
     // ---------------- W3: synchronization (Alg 3; vanilla P:788)
     unsigned selmask[KS];
 #pragma unroll
@@ -666,6 +789,7 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
         __syncwarp();
       }
     }
+    SF_CK(1);
     // ---------------- W4: migration (Alg 4), StaleFlow only (vanilla: none)
     if (sf_mig) {
       int k1[KS];
@@ -735,8 +859,10 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
         __syncwarp();
       }
     }
+    SF_CK(2);
     // ---------------- W5: routing (Alg 2) over the TS incl. interrupted trajectories
     c.n_v = build_mlq(P, D, C, c, sg, &min_v);
+    SF_CK(3);
     if (min_v < 0) c.mlq_err = 1;
 #ifdef SF_TIMING
     const long long t_rp = clock64();
@@ -747,6 +873,7 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
 #endif
     m_routes = nr;
     m_reserves = c.reserves;
+    SF_CK(4);
     // write back per-instance route effects (Table 1 Route row)
 #pragma unroll
     for (int q = 0; q < KS; ++q) {
@@ -775,6 +902,7 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
         if (n > 0) order_arrivals_global(P, D, C, c, i, n);
       }
     }
+    SF_CK(5);
   } else {
     m_invalid = 1;
   }
@@ -799,12 +927,7 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
     if (D.dbg) {
       D.dbg[8 * s + 0] = clock64() - t0_clk;
       D.dbg[8 * s + 1] = m_routes;
-      D.dbg[8 * s + 2] = m_interrupts;
-      D.dbg[8 * s + 3] = m_pulls;
-      D.dbg[8 * s + 4] = m_valid;
-      D.dbg[8 * s + 5] = c.n_v;
-      D.dbg[8 * s + 6] = c.n_vl;
-      D.dbg[8 * s + 7] = dbg_tent;
+      for (int q = 0; q < 6; ++q) D.dbg[8 * s + 2 + q] = ck[q];
     }
 #endif
   }

@@ -200,7 +200,7 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
     S.ev_off = ev; S.batch_off = batch; S.cmd_off = cmd;
     c->max_inst = std::max(c->max_inst, S.I);
     inst += S.I; led += (long long)(S.eta + 1) * B; ring += S.eta + 1; list += (long long)S.I * S.cap;
-    bits += bwords; mlq += 2LL * S.cap; ev += S.cap; batch += batch_rec; cmd += 4LL * P.cmdlog_cap;
+    bits += bwords; mlq += 3LL * S.cap + 2; ev += S.cap; batch += batch_rec; cmd += 4LL * P.cmdlog_cap;
   }
   c->n_inst_total = (int)inst;
   // launch mode: the three-kernel path by default (measured faster on C5);
