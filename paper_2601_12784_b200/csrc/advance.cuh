@@ -86,16 +86,37 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
       tq[q] = D.T[C.traj_off + rid[q]];
       fin[q] = D.prompt[C.grp_off + grp_of(P, rid[q])] + tq[q];
     }
-  // arrivals 0..31 of this window: lane k holds arrival k
-  int a_id = 0, a_gen = 0, a_T = 0, a_p = 0;
-  if ((int)lane < x.arr_n) {
-    a_id = D.arr_id[lb + lane];
-    const long long j = C.traj_off + a_id;
-    a_gen = D.gen[j]; a_T = D.T[j]; a_p = D.prompt[C.grp_off + grp_of(P, a_id)];
-  }
+  // Arrivals are read through two 32-wide register windows, each refilled with one coalesced
+  // load per 32 arrivals: window 6 (id, t_arr) for delivery in B6, window 7 (id, gen, T, prompt)
+  // for admission in B7.  Lane k of a window holds arrival base + k.
+  int b6 = 0, a6_id = 0, b7 = 0, a7_id = 0, a7_gen = 0, a7_T = 0, a7_p = 0;
+  long long a6_t = kInf;
+  auto load6 = [&](int base) {
+    b6 = base;
+    const int k = base + (int)lane;
+    a6_id = 0; a6_t = kInf;
+    if (k < x.arr_n) { a6_id = D.arr_id[lb + k]; a6_t = D.arr_t[lb + k]; }
+  };
+  auto load7 = [&](int base) {
+    b7 = base;
+    const int k = base + (int)lane;
+    a7_id = 0; a7_gen = 0; a7_T = 0; a7_p = 0;
+    if (k < x.arr_n) {
+      a7_id = D.arr_id[lb + k];
+      const long long j = C.traj_off + a7_id;
+      a7_gen = D.gen[j]; a7_T = D.T[j]; a7_p = D.prompt[C.grp_off + grp_of(P, a7_id)];
+    }
+  };
+  if (x.arr_n > 0) { load6(0); load7(0); }
   int arr_ring0 = -1;                       // wait-ring position of arrival 0 once appended
   int nlive = x.run_n, tail = x.run_n, n_ev = 0;
-  long long next_arr = x.arr_head < x.arr_n ? D.arr_t[lb + x.arr_head] : kInf;
+  // arrival k's time (k only grows): window 6, refilled when k leaves it
+  auto arr_time = [&](int k) -> long long {
+    if (k >= x.arr_n) return kInf;
+    if (k >= b6 + 32) load6(k);
+    return __shfl_sync(0xffffffffu, a6_t, k - b6);
+  };
+  long long next_arr = arr_time(x.arr_head);
   bool head_ok = false, blocked = false;
   int head_id = 0, head_gen = 0, head_T = 0;
   long long head_ctx = 0;
@@ -229,14 +250,15 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
     if (next_arr <= b) {
       if (x.wn == 0) { head_ok = false; blocked = false; }
       do {
-        const int id = D.arr_id[lb + x.arr_head];
+        if (x.arr_head >= b6 + 32) load6(x.arr_head);
+        const int id = __shfl_sync(0xffffffffu, a6_id, x.arr_head - b6);
         int pos = x.whead + x.wn;
         if (pos >= cap) pos -= cap;
         if (x.arr_head == 0) arr_ring0 = pos;
         if (lane == 0) { D.wait_id[lb + pos] = id; D.loc[C.traj_off + id] = L_WAIT; }
         ++x.wn;
         ++x.arr_head;
-        next_arr = x.arr_head < x.arr_n ? D.arr_t[lb + x.arr_head] : kInf;
+        next_arr = arr_time(x.arr_head);
       } while (next_arr <= b);
       __syncwarp();
     }
@@ -249,13 +271,14 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
           if (arr_ring0 >= 0) {
             k = x.whead - arr_ring0;
             if (k < 0) k += cap;
-            if (k >= x.arr_head || k >= 32) k = -1;
+            if (k >= x.arr_head || k < b7) k = -1;
           }
           if (k >= 0) {
-            head_id = __shfl_sync(0xffffffffu, a_id, k);
-            head_gen = __shfl_sync(0xffffffffu, a_gen, k);
-            head_T = __shfl_sync(0xffffffffu, a_T, k);
-            head_ctx = __shfl_sync(0xffffffffu, a_p, k) + head_gen;
+            if (k >= b7 + 32) load7(k);
+            head_id = __shfl_sync(0xffffffffu, a7_id, k - b7);
+            head_gen = __shfl_sync(0xffffffffu, a7_gen, k - b7);
+            head_T = __shfl_sync(0xffffffffu, a7_T, k - b7);
+            head_ctx = __shfl_sync(0xffffffffu, a7_p, k - b7) + head_gen;
           } else {
             head_id = D.wait_id[lb + x.whead];
             const long long j = C.traj_off + head_id;
@@ -323,23 +346,58 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
     // Quiet decode steps: the next boundary is a step end with no pending command, no
     // completion (no live rem == 1), no preemption (kv + k5 n <= M), no arrival due, and no
     // admission possible (B7 just left the head blocked or the queue empty).  Such a boundary
-    // only credits the step (B2) and starts the next one (B8); do exactly that, in registers.
+    // only credits the step (B2) and starts the next one (B8).
     if (x.intkind == INT_NONE && !x.pullpend) {
       const int k5n = (int)(k5 * nlive);
-      for (;;) {
-        const long long bq = x.nb;
-        if (bq > t_end || x.kv + k5n > P.M || next_arr <= bq) break;
-        unsigned one = 0;
+      if (P.skip) {
+        // f1: jump over the whole run of quiet steps in closed form.  With
+        // kv0 = kv at the current step start and c1 = k1 kv0 + cn, the j-th quiet boundary is
+        //   b_j = nb + (j-1) c1 + k1 k5n (j-1) j / 2            (Eq 7 with kv growing k5 n per step)
+        // and boundary j is quiet iff j <= minrem - 1, kv0 + j k5n <= M, b_j <= t_end and
+        // b_j < next arrival.  m = the largest such j (binary search on the exact int128 b_j).
+        int mr = kDead;
 #pragma unroll
-        for (int q = 0; q < kR; ++q) one |= __ballot_sync(0xffffffffu, rem[q] == 1);
-        if (one) break;
+        for (int q = 0; q < kR; ++q) mr = min(mr, rem[q]);
+        mr = warp_min(mr);
+        long long m_hi = (long long)mr - 1;
+        m_hi = min(m_hi, (P.M - x.kv) / k5n);
+        const long long t_lim = min(t_end, next_arr - 1);
+        const __int128 kv0 = x.kv, nb0 = x.nb;
+        const __int128 c1 = (__int128)P.k1i * kv0 + cn, q1 = (__int128)P.k1i * k5n;
+        long long lo = 0, hi = max(m_hi, 0LL);
+        while (lo < hi) {                                       // largest j in [0, hi] with b_j <= t_lim
+          const long long mid = (lo + hi + 1) >> 1;
+          const __int128 bj = nb0 + (__int128)(mid - 1) * c1 + q1 * (__int128)((mid - 1) * mid / 2);
+          if (bj <= t_lim) lo = mid; else hi = mid - 1;
+        }
+        const long long m = lo;
+        if (m > 0) {
 #pragma unroll
-        for (int q = 0; q < kR; ++q) rem[q] -= 1;
-        x.kv += k5n;
-        x.tokens += nlive;
-        x.nb = bq + (long long)P.k1i * (int)x.kv + cn;
-        x.iters += nlive;
-        ++x.ticks;
+          for (int q = 0; q < kR; ++q) rem[q] -= (int)m;
+          x.kv += m * k5n;
+          x.tokens += m * nlive;
+          x.iters += m * nlive;
+          x.ticks += m;
+          // b_{m+1} = b_m + k1 (kv0 + m k5n) + cn
+          const __int128 bm = nb0 + (__int128)(m - 1) * c1 + q1 * (__int128)((m - 1) * m / 2);
+          x.nb = (long long)(bm + (__int128)P.k1i * (kv0 + (__int128)m * k5n) + cn);
+        }
+      } else {
+        for (;;) {
+          const long long bq = x.nb;
+          if (bq > t_end || x.kv + k5n > P.M || next_arr <= bq) break;
+          unsigned one = 0;
+#pragma unroll
+          for (int q = 0; q < kR; ++q) one |= __ballot_sync(0xffffffffu, rem[q] == 1);
+          if (one) break;
+#pragma unroll
+          for (int q = 0; q < kR; ++q) rem[q] -= 1;
+          x.kv += k5n;
+          x.tokens += nlive;
+          x.nb = bq + (long long)P.k1i * (int)x.kv + cn;
+          x.iters += nlive;
+          ++x.ticks;
+        }
       }
     }
   }
@@ -480,6 +538,9 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
 // One window of W6-W7 for global instance gi, executed by one warp (stage: 32*kR int2 of smem).
 __device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D, int gi, AdvStage &stage) {
   const unsigned lane = lane_id();
+#ifdef SF_TIMING
+  const long long t0_adv = clock64();
+#endif
   const int s = D.inst_scen[gi];
   const ScenConst C = D.sc[s];
   ScenState &SS = D.ss[s];
@@ -525,6 +586,13 @@ __device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D,
     metric_add(SS, M_TOKENS, x.tokens);
     metric_add(SS, M_COMPLETIONS, x.comps);
     metric_add(SS, M_PREEMPTIONS, x.preempts);
+#ifdef SF_TIMING
+    if (D.dbg2) {
+      long long *r = D.dbg2 + 8LL * gi;
+      r[0] = clock64() - t0_adv; r[1] = x.ticks; r[2] = x.comps; r[3] = x.arr_n; r[4] = x.preempts;
+      r[5] = x.run_n; r[6] = x.wn; r[7] = x.iters;
+    }
+#endif
   }
 }
 

@@ -4,7 +4,10 @@
 
 namespace sf {
 
-__global__ void __launch_bounds__(32 * kWarpsPerBlock) k_advance(GParams P, Dev D, int n_inst_total) {
+#ifndef SF_ADV_MINB
+#define SF_ADV_MINB 2      // measured best: 2 blocks x 8 warps per SM (128 registers, no spills)
+#endif
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, SF_ADV_MINB) k_advance(GParams P, Dev D, int n_inst_total) {
   __shared__ AdvStage stage_all[kWarpsPerBlock];
   const int gi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (gi >= n_inst_total) return;

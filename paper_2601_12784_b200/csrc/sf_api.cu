@@ -206,6 +206,10 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
   // launch mode: the three-kernel path by default (measured faster on C5);
   // SF_LAUNCH=fused selects the fused per-scenario window kernel (tests run both)
   c->fused = 0;
+  // decode-step mode: closed-form skipping of quiet steps by default;
+  // SF_ADVANCE=step processes every decode step individually (tests run both)
+  c->P.skip = 1;
+  if (const char *m = getenv("SF_ADVANCE")) c->P.skip = strcmp(m, "step") != 0;
   if (const char *m = getenv("SF_LAUNCH")) {
     if (!strcmp(m, "split")) c->fused = 0;
     if (!strcmp(m, "fused")) c->fused = c->max_inst <= 32;
@@ -240,9 +244,10 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
     return SF_E_NOMEM;
   }
 #ifdef SF_TIMING
-  ok = dalloc(c, &D.dbg, 8LL * ns, 0);
+  ok = dalloc(c, &D.dbg, 8LL * ns, 0) && dalloc(c, &D.dbg2, 8LL * inst, 0);
 #else
   D.dbg = nullptr;
+  D.dbg2 = nullptr;
 #endif
   D.sc = dsc;
   D.ss = dss;
@@ -569,6 +574,11 @@ int64_t sf_kernel_launches(const sf_ctx *c) { return c ? c->launches : 0; }
 sf_status sf_debug_coord_cycles(sf_ctx *c, int64_t *out) {
   if (!c || !c->D.dbg) return SF_E_INVALID;
   cudaMemcpy(out, c->D.dbg, 8 * sizeof(long long) * c->n_scen, cudaMemcpyDeviceToHost);
+  return SF_OK;
+}
+sf_status sf_debug_adv_cycles(sf_ctx *c, int64_t *out) {
+  if (!c || !c->D.dbg2) return SF_E_INVALID;
+  cudaMemcpy(out, c->D.dbg2, 8 * sizeof(long long) * c->n_inst_total, cudaMemcpyDeviceToHost);
   return SF_OK;
 }
 #endif

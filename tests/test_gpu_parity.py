@@ -16,13 +16,16 @@ from tests.parity import compare, make_pair, run_lockstep, submit_both
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["auto", "fused"])
+@pytest.fixture(params=["auto", "fused", "step"])
 def launch_mode(request, monkeypatch):
-    """Both launch modes (three kernels / fused window kernel) must give identical results."""
-    if request.param != "auto":
-        monkeypatch.setenv("SF_LAUNCH", request.param)
-    else:
-        monkeypatch.delenv("SF_LAUNCH", raising=False)
+    """Every launch / decode-step mode must give identical results: default (three kernels,
+    closed-form quiet steps), fused window kernel, and one-by-one decode steps."""
+    monkeypatch.delenv("SF_LAUNCH", raising=False)
+    monkeypatch.delenv("SF_ADVANCE", raising=False)
+    if request.param == "fused":
+        monkeypatch.setenv("SF_LAUNCH", "fused")
+    if request.param == "step":
+        monkeypatch.setenv("SF_ADVANCE", "step")
     return request.param
 
 
