@@ -268,6 +268,33 @@ def main():
     if not args.no_e2e and not args.profile_run:
         e2e = run_e2e(args, full, idx, stream, world, barrier)
 
+    # ---------------- supplementary: the same K windows as ONE sf_step call (fused kernel: each
+    # scenario's warp runs all K windows without a grid-wide barrier per window; L2 not flushed
+    # between windows because there is no host boundary).  Not the headline.
+    multi = None
+    if not args.profile_run and not args.no_e2e:
+        os.environ["SF_LAUNCH"] = "fused"
+        ctx2 = StaleFlow.from_preset(p, stream=stream)
+        os.environ.pop("SF_LAUNCH", None)
+        assert ctx2.submit_many(np.arange(S), np.full(S, full.pool_groups), pr, tg) == 0
+        ctx2.step(args.warmup)
+        barrier()
+        n0 = ctx2.metrics()[2]
+        s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s2.record(stream)
+        ctx2.step(args.steps)
+        e2.record(stream)
+        barrier()
+        it2 = torch.tensor([int(ctx2.metrics()[2] - n0)], dtype=torch.int64, device="cuda")
+        ms2 = torch.tensor([s2.elapsed_time(e2)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(it2, op=dist.ReduceOp.SUM)
+            dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
+        multi = {"value": int(it2.item()) / (float(ms2.item()) / 1e3), "unit": UNIT,
+                 "windows_per_call": args.steps, "launch": "fused (k_window), 1 launch",
+                 "ms_per_window": float(ms2.item()) / args.steps}
+        ctx2.close()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile_run:
         cpu = oracle_rate(full, idx, args.warmup, args.steps, args.cpu_seconds)
@@ -289,6 +316,7 @@ def main():
                          "step_share": share},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "multi_window": multi,
             "gpu_launches": int(launches),
             "clocks": clk,
             "sim": {"routes": int(dm[5].item()), "completions": int(dm[4].item()), "batches": int(dm[9].item()),
