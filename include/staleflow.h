@@ -147,6 +147,26 @@ int64_t sf_kernel_launches(const sf_ctx *ctx);
 sf_status sf_profile(sf_ctx *ctx, int32_t enable);
 sf_status sf_profile_read(sf_ctx *ctx, double *ms, int64_t *launches, int32_t len);
 
+/* ---- host-side tools adjacent to the step; no context needed ---- */
+
+/* Least-squares fit of Eq 7 ("offline profiling and linear regression", P:636,
+ * 1071): latency = k1*kv + max(k2, k3*n) + k4 from n_samples (kv, n_run, latency) samples, the
+ * max() handled by iterated regime segmentation (<= 50 rounds).  k_out[4] = k1, k2, k3, k4 in the
+ * samples' units.  SF_E_INVALID if n_samples < 4; SF_E_STATE if degenerate (rank deficient, e.g.
+ * every sample in one regime). */
+sf_status sf_fit_cost_model(int32_t n_samples, const double *kv, const double *n_run, const double *latency,
+                            double *k_out);
+
+/* Load-balancing communication plan for Push (App A.2; fig:comm): for each
+ * requirement r (slice req_slice[r] needed by receiver req_receiver[r], input order), choose the
+ * sender holding the slice with the smallest accumulated latency estimate (ties: lowest id) and
+ * add slice_bytes / bandwidth + latency of that (sender, receiver) pair.  holds[n_senders *
+ * n_slices] (0/1), bandwidth / latency [n_senders * n_receivers].  Writes out_sender[n_req] and
+ * acc[n_senders].  SF_E_INVALID if a required slice has no holder. */
+sf_status sf_plan_comm(int32_t n_slices, const double *slice_bytes, int32_t n_senders, int32_t n_receivers,
+                       const uint8_t *holds, const double *bandwidth, const double *latency, int32_t n_req,
+                       const int32_t *req_slice, const int32_t *req_receiver, int32_t *out_sender, double *acc);
+
 /* Message for the last failing call; owned by the context, valid until the next call. */
 const char *sf_last_error(const sf_ctx *ctx);
 

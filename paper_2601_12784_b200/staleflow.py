@@ -26,7 +26,8 @@ STATUS = {0: "SF_OK", 1: "SF_NOT_READY", -1: "SF_E_INVALID", -2: "SF_E_VERSION",
 EXPORTS = ["sf_create", "sf_destroy", "sf_submit_prompts", "sf_submit_prompts_many", "sf_step",
            "sf_publish_params", "sf_collect_batch", "sf_read_metrics", "sf_read_metrics_device",
            "sf_read_scenario_metrics", "sf_read_all_scenario_metrics", "sf_dump_lifecycles", "sf_dump_batches", "sf_dump_commands",
-           "sf_dump_instances", "sf_kernel_launches", "sf_last_error", "sf_profile", "sf_profile_read"]
+           "sf_dump_instances", "sf_kernel_launches", "sf_last_error", "sf_profile", "sf_profile_read",
+           "sf_fit_cost_model", "sf_plan_comm"]
 
 
 class SfConfig(C.Structure):
@@ -83,6 +84,11 @@ def load_library(path: str = LIB_PATH):
         "sf_kernel_launches": (I64, [P]),
         "sf_last_error": (C.c_char_p, [P]),
         "sf_profile": (C.c_int, [P, I32]),
+        "sf_fit_cost_model": (C.c_int, [I32, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                        C.POINTER(C.c_double)]),
+        "sf_plan_comm": (C.c_int, [I32, C.POINTER(C.c_double), I32, I32, C.POINTER(C.c_uint8),
+                                   C.POINTER(C.c_double), C.POINTER(C.c_double), I32, pI32, pI32, pI32,
+                                   C.POINTER(C.c_double)]),
         "sf_profile_read": (C.c_int, [P, C.POINTER(C.c_double), pI64, I32]),
     }
     for name, (res, args) in sig.items():
@@ -267,3 +273,38 @@ class StaleFlow:
     @property
     def kernel_launches(self) -> int:
         return int(self.L.sf_kernel_launches(self.h))
+
+
+# ---------------------------------------------------------------- host-side tools (f4)
+def fit_cost_model(kv, n_run, latency):
+    """sf_fit_cost_model: (k1, k2, k3, k4) of Eq 7 from profile samples."""
+    L = load_library()
+    kv = np.ascontiguousarray(kv, np.float64)
+    n_run = np.ascontiguousarray(n_run, np.float64)
+    latency = np.ascontiguousarray(latency, np.float64)
+    out = np.zeros(4, np.float64)
+    rc = L.sf_fit_cost_model(len(kv), _p(kv, C.c_double), _p(n_run, C.c_double), _p(latency, C.c_double),
+                             _p(out, C.c_double))
+    if rc != 0:
+        raise SfError(f"sf_fit_cost_model: {STATUS.get(rc, rc)}")
+    return out
+
+
+def plan_comm(slice_bytes, holds, bandwidth, latency, req_slice, req_receiver):
+    """sf_plan_comm: (sender per requirement, accumulated estimate per sender)."""
+    L = load_library()
+    sb = np.ascontiguousarray(slice_bytes, np.float64)
+    h = np.ascontiguousarray(holds, np.uint8)
+    bw = np.ascontiguousarray(bandwidth, np.float64)
+    lt = np.ascontiguousarray(latency, np.float64)
+    rs = np.ascontiguousarray(req_slice, np.int32)
+    rr = np.ascontiguousarray(req_receiver, np.int32)
+    n_senders, n_receivers = bw.shape
+    out = np.zeros(max(1, len(rs)), np.int32)
+    acc = np.zeros(n_senders, np.float64)
+    rc = L.sf_plan_comm(len(sb), _p(sb, C.c_double), n_senders, n_receivers, _p(h, C.c_uint8), _p(bw, C.c_double),
+                        _p(lt, C.c_double), len(rs), _p(rs, C.c_int32), _p(rr, C.c_int32), _p(out, C.c_int32),
+                        _p(acc, C.c_double))
+    if rc != 0:
+        raise SfError(f"sf_plan_comm: {STATUS.get(rc, rc)}")
+    return out[: len(rs)], acc
