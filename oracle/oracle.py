@@ -23,7 +23,7 @@ METRIC_NAMES = [
     "preemptions", "batches", "valid_snapshots", "invalid_snapshots", "violations", "publishes",
     "ingested_groups", "occupied_groups",
     "stale_0", "stale_1", "stale_2", "stale_3", "stale_4", "stale_5", "stale_6", "stale_7", "stale_8+",
-    "command_hash", "sim_time_ps", "reserves", "relocations", "poisoned_scenarios", "max_sim_time_ps", "rsv31",
+    "command_hash", "sim_time_ps", "reserves", "relocations", "poisoned_scenarios", "max_sim_time_ps", "aborts",
 ]
 
 _lock = threading.Lock()
@@ -54,6 +54,7 @@ class Config(C.Structure):
         ("mu", C.c_double), ("phi_tp", C.c_double), ("phi_wait", C.c_int32),
         ("delta", C.c_int64), ("r", C.c_int64), ("q", C.c_int64), ("R", C.c_int64),
         ("strategy", C.c_uint32), ("atw", C.c_int32), ("pool_capacity_groups", C.c_int32),
+        ("extra_groups", C.c_int32), ("extra_members", C.c_int32),
     ]
 
 
@@ -93,6 +94,8 @@ def load_oracle():
         "sfo_dump_commands": (C.c_int, [P, I32, pI64, I64, pI64]),
         "sfo_dump_instances": (C.c_int, [P, I32, pI64, I64, pI64]),
         "sfo_ledger_new": (P, [I32, I32]),
+        "sfo_ledger_new2": (P, [I32, I32, I32]),
+        "sfo_ledger_consume2": (C.c_int, [P, pI32, pI32, pI32, pI32]),
         "sfo_ledger_free": (None, [P]),
         "sfo_ledger_clone": (P, [P]),
         "sfo_ledger_verify": (C.c_int, [P, I32]),
@@ -139,7 +142,8 @@ def oracle_config_from_preset(p, scen_idx: Optional[Sequence[int]] = None):
                  k5=p.k5, kp=p.kprefill_ps, M=p.kv_budget, mu=p.mu, phi_tp=p.phi_tp, phi_wait=p.phi_wait,
                  delta=p.snap_period_ps, r=p.route_lat_ps, q=p.pull_lat_ps, R=p.reward_lat_ps,
                  strategy=scs[0].strategy, atw=p.auto_train_windows,
-                 pool_capacity_groups=getattr(p, "pool_capacity", None) or p.pool_groups)
+                 pool_capacity_groups=getattr(p, "pool_capacity", None) or p.pool_groups,
+                 extra_groups=getattr(p, "extra_groups", 0), extra_members=getattr(p, "extra_members", 0))
     return int(inst[0]), int(eta[0]), p.group_size, cfg, (eta, inst, strat)
 
 
@@ -236,10 +240,11 @@ class OracleSim:
 class Ledger:
     """Wrapper over the oracle's staleness ledger (§4.2) for unit pins."""
 
-    def __init__(self, eta: int, B: int, _h=None):
+    def __init__(self, eta: int, B: int, _h=None, capacity: int = None):
         self.L = load_oracle()
         self.eta, self.B = eta, B
-        self.h = _h if _h is not None else self.L.sfo_ledger_new(eta, B)
+        self.cap = capacity or B
+        self.h = _h if _h is not None else self.L.sfo_ledger_new2(eta, self.cap, B)
 
     def __del__(self):
         try:
@@ -249,7 +254,7 @@ class Ledger:
             pass
 
     def clone(self):
-        return Ledger(self.eta, self.B, self.L.sfo_ledger_clone(self.h))
+        return Ledger(self.eta, self.B, self.L.sfo_ledger_clone(self.h), capacity=self.cap)
 
     def verify(self, v: int) -> bool:
         return bool(self.L.sfo_ledger_verify(self.h, v))
@@ -281,7 +286,15 @@ class Ledger:
         rc = self.L.sfo_ledger_consume(self.h, _ptr(g, C.c_int32), _ptr(v, C.c_int32))
         return rc, g, v
 
-    def get(self, b: int, s: int):
+    def consume_surplus(self):
+        g = np.zeros(self.B, np.int32)
+        v = np.zeros(self.B, np.int32)
+        sp = np.zeros(self.cap, np.int32)
+        n = C.c_int32()
+        rc = self.L.sfo_ledger_consume2(self.h, _ptr(g, C.c_int32), _ptr(v, C.c_int32), _ptr(sp, C.c_int32), C.byref(n))
+        return rc, g, v, sp[: n.value]
+
+    def get(self, b: int, s: int):  # noqa: D401
         st, g, v = C.c_int32(), C.c_int32(), C.c_int32()
         self.L.sfo_ledger_get(self.h, b, s, C.byref(st), C.byref(g), C.byref(v))
         return (["Empty", "Reserved", "Occupied"][st.value], g.value, v.value)
@@ -291,7 +304,7 @@ class Ledger:
         return self.L.sfo_ledger_cu(self.h)
 
     def entries(self, nbuf: int):
-        return [[self.get(b, s) for s in range(self.B)] for b in range(nbuf)]
+        return [[self.get(b, s) for s in range(self.cap)] for b in range(nbuf)]
 
 
 def make_params(eta=1, k1=None, k2=None, k3=None, k4=None, k5=1, kp=0, M=1 << 40, mu=0.3, phi_tp=5.0,

@@ -29,6 +29,7 @@ struct Entry { int st = E_EMPTY; int g = -1; int v = -1; };
 
 struct sfo_ledger {
   int eta = 0, B = 1;
+  int Br = 1;                                  // batch size: Ready at >= Br Occupied (App C redundancy)
   int cu = 0;                                  // consumed_upto: earliest unconsumed V_buf
   std::vector<std::vector<Entry>> buf;         // buf[V_buf], all Empty until touched
 
@@ -106,11 +107,14 @@ struct sfo_ledger {
     }
     return false;
   }
-  // Buffer states: Waiting (>= 1 empty), Ready (all occupied), Stuck (full, >= 1 reserved).
+  // Buffer states: Ready (all occupied; under batch-level redundancy >= Br occupied,
+  // S:41), Waiting (>= 1 empty), Stuck (full with >= 1 reserved).
   int state(int b) const {
-    if (has_empty(b)) return 0;
-    for (int s = 0; s < B; ++s) if (buf[b][s].st != E_OCCUPIED) return 2;
-    return 1;
+    int occ = 0;
+    if (b < (int)buf.size())
+      for (int s = 0; s < B; ++s) occ += buf[b][s].st == E_OCCUPIED;
+    if (occ >= Br) return 1;
+    return has_empty(b) ? 0 : 2;
   }
 };
 
@@ -294,19 +298,20 @@ void migrate(const Params &P, const std::vector<View> &S0, std::vector<int> &cas
 
 // ============================================================== discrete-event simulation
 namespace {
-enum { L_POOL = 0, L_TS = 1, L_TRANSIT = 2, L_WAIT = 3, L_RUN = 4, L_DONE = 5, L_CONSUMED = 6 };
+enum { L_POOL = 0, L_TS = 1, L_TRANSIT = 2, L_WAIT = 3, L_RUN = 4, L_DONE = 5, L_CONSUMED = 6, L_ABORTED = 7 };
 enum { I_IDLE = 0, I_TICK = 1, I_PULL = 2 };
-enum { CMD_ROUTE = 1, CMD_INTERRUPT = 2, CMD_PULL = 3 };
+enum { CMD_ROUTE = 1, CMD_INTERRUPT = 2, CMD_PULL = 3, CMD_ABORT = 4 };
 enum {
   M_WINDOWS = 0, M_TICKS, M_TRAJ_ITERS, M_TOKENS, M_COMPLETIONS, M_ROUTES, M_INTERRUPTS, M_PULLS,
   M_PREEMPTIONS, M_BATCHES, M_VALID_SNAP, M_INVALID_SNAP, M_VIOLATIONS, M_PUBLISHES, M_INGESTED,
   M_OCCUPIED, M_HIST0 /* ..M_HIST0+8 */, M_CMD_HASH = 25, M_SIM_TIME = 26, M_RESERVES = 27,
-  M_RELOCATIONS = 28
+  M_RELOCATIONS = 28, M_ABORTS = 31
 };
 const int64_t INF = std::numeric_limits<int64_t>::max();
 
 struct Traj {
   int g = 0, T = 0, gen = 0, st = L_POOL, inst = -1;
+  bool rewarded = false;
   int n_routes = 0, n_preempt = 0, n_interrupt = 0;
   int64_t t_complete = -1, ready = 0;
 };
@@ -317,6 +322,7 @@ struct Inst {
   int st = I_IDLE; int64_t nb = 0, pull_until = 0; int pull_version = 0;
   bool pull_pending = false, cmd_at_t = false;
   std::vector<std::pair<int, int64_t>> interrupt_set;   // (trajectory, context held here at issue)
+  std::vector<int> abort_set;                           // pending Abort commands (run / wait members)
   std::vector<Arrival> arrivals;
   int64_t prefill = 0;
   int pv = 0, acc = 0;                   // speculative state P[i], initialised to 0
@@ -326,6 +332,7 @@ struct Ev { int64_t t; int id; };
 struct Scen {
   Params P;
   int I = 0, eta = 0, B = 0, G = 0; uint32_t strategy = 0;
+  int Br = 0, Gr = 0;              // batch size and required members; B, G include redundancy (App C)
   int64_t delta = 0, r = 0, q = 0, R = 0; int atw = 0; int pool_cap = 0;
   std::vector<Traj> traj; std::vector<Group> grp;
   int n_pool = 0, n_ingested = 0, live = 0;
@@ -351,25 +358,56 @@ void log_cmd(Scen &s, int kind, int inst, int traj) {
 }
 int ctx_len(const Scen &s, int j) { return s.grp[s.traj[j].g].p + s.traj[j].gen; }
 
-// Consume: retire the earliest Ready buffer as one batch; staleness check (A30).
+// Abort (P:473 footnote; Table 1 row P:577): trajectory j leaves for good.  On an instance it is
+// removed at that instance's next boundary; an arrival in transit is dropped at delivery; a
+// TS-resident one is dropped from the TS; a completed one's pending reward is ignored.
+void abort_member(Scen &s, int j) {
+  Traj &tr = s.traj[j];
+  const int st = tr.st;
+  if (st == L_ABORTED || st == L_CONSUMED || tr.rewarded) return;
+  if (st == L_TRANSIT || st == L_WAIT || st == L_RUN) {
+    log_cmd(s, CMD_ABORT, tr.inst, j);
+    s.inst[tr.inst].acc -= 1;
+    if (s.inst[tr.inst].acc < 0) s.err = SFO_E_STATE;
+    if (st != L_TRANSIT) s.inst[tr.inst].abort_set.push_back(j);
+  }
+  tr.st = L_ABORTED;
+  s.m[M_ABORTS]++;
+}
+
+void abort_group(Scen &s, int g) {
+  for (int m = 0; m < s.G; ++m) abort_member(s, g * s.G + m);
+}
+
+// Consume: retire the earliest Ready buffer as one batch -- its first Br Occupied entries in
+// slot order; surplus entries (Occupied beyond Br, and Reserved) are aborted (App C).
+// Staleness check (A30).
 void consume(Scen &s, int *vbuf, int *gids, int *gv) {
   int cu = s.L.cu;
   if (vbuf) *vbuf = cu;
   s.batches.push_back(cu);
+  int taken = 0, nonempty = 0;
+  std::vector<int> surplus;
   for (int k = 0; k < s.B; ++k) {
     const Entry &e = s.L.buf[cu][k];
+    if (e.st == E_EMPTY) continue;
+    ++nonempty;
+    if (e.st != E_OCCUPIED || taken == s.Br) { surplus.push_back(e.g); continue; }
     int stal = cu - e.v;
     if (stal < 0 || stal > s.eta) { s.m[M_VIOLATIONS]++; s.err = SFO_E_STATE; }
     s.m[M_HIST0 + std::min(std::max(stal, 0), 8)]++;
     s.grp[e.g].consumed_vbuf = cu;
-    for (int m = 0; m < s.G; ++m) s.traj[e.g * s.G + m].st = L_CONSUMED;
+    for (int m = 0; m < s.G; ++m)
+      if (s.traj[e.g * s.G + m].rewarded) s.traj[e.g * s.G + m].st = L_CONSUMED;
     s.batches.push_back(e.g);
     s.batches.push_back(e.v);
-    if (gids) gids[k] = e.g;
-    if (gv) gv[k] = e.v;
+    if (gids) gids[taken] = e.g;
+    if (gv) gv[taken] = e.v;
+    ++taken;
   }
+  for (int g : surplus) abort_group(s, g);
   s.L.cu = cu + 1;
-  s.live -= s.B;
+  s.live -= nonempty;
   s.m[M_BATCHES]++;
 }
 
@@ -481,6 +519,17 @@ void boundary(Scen &s, int i, int64_t b) {
     }
     n.interrupt_set.clear();
   }
+  // B1 (Abort): removed like an interrupt, but the trajectory does not return to the TS.
+  if (n.st != I_PULL && !n.abort_set.empty()) {
+    for (int j : n.abort_set) {
+      auto it = std::find(n.run.begin(), n.run.end(), j);
+      if (it != n.run.end()) { n.kv -= (int64_t)P.k5 * ctx_len(s, j); n.run.erase(it); continue; }
+      auto jt = std::find(n.wait.begin(), n.wait.end(), j);
+      if (jt != n.wait.end()) { n.wait.erase(jt); continue; }
+      s.err = SFO_E_STATE;
+    }
+    n.abort_set.clear();
+  }
   if (tick_end) {
     // B2: one token for every remaining tick member (batched decode).
     for (int j : n.run) { s.traj[j].gen += 1; n.kv += P.k5; s.m[M_TOKENS]++; }
@@ -524,8 +573,8 @@ void boundary(Scen &s, int i, int64_t b) {
   });
   std::vector<Arrival> later;
   for (const Arrival &a : n.arrivals) {
-    if (a.t <= b) { n.wait.push_back(a.id); s.traj[a.id].st = L_WAIT; }
-    else later.push_back(a);
+    if (a.t > b) later.push_back(a);
+    else if (s.traj[a.id].st != L_ABORTED) { n.wait.push_back(a.id); s.traj[a.id].st = L_WAIT; }
   }
   n.arrivals = later;
   // B7: FIFO admission while the head fits in the KV budget (Eq 3's gamma rule).
@@ -569,10 +618,14 @@ int64_t next_boundary(const Scen &s, const Inst &n) {
 
 // Staleness-manager side of a completed reward.
 void apply_reward(Scen &s, int j) {
+  if (s.traj[j].st == L_ABORTED) return;    // aborted after completing: the reward is ignored
   int g = s.traj[j].g;
   Group &gr = s.grp[g];
+  s.traj[j].rewarded = true;
   gr.n_rewarded += 1;
-  if (gr.n_rewarded < s.G) return;          // group sampling: occupy only when all complete
+  if (gr.n_rewarded < s.Gr) return;         // group sampling: occupy when Gr members complete
+  // group-level redundancy: the surplus members are aborted the moment the group completes
+  for (int m = 0; m < s.G; ++m) abort_member(s, g * s.G + m);
   int b = -1, sl = -1;
   if (!s.L.find(g, &b, &sl) || s.L.buf[b][sl].st != E_RESERVED) { s.err = SFO_E_STATE; return; }
   s.m[M_RELOCATIONS] += s.L.delete_and_relocate(b, sl);
@@ -595,7 +648,7 @@ void run_window(Scen &s) {
     }
   }
   // W1: TS ingest up to (eta+1) x batch_size live groups (A23).
-  while (s.live < (s.eta + 1) * s.B && s.n_ingested < s.n_pool) {
+  while (s.live < (s.eta + 1) * s.B && s.n_ingested < s.n_pool) {   // B includes extra groups
     int g = s.n_ingested++;
     s.live++;
     s.m[M_INGESTED]++;
@@ -605,7 +658,8 @@ void run_window(Scen &s) {
   bool valid = true;
   for (int i = 0; i < s.I; ++i) {
     const Inst &n = s.inst[i];
-    bool quiescent = n.interrupt_set.empty() && !n.pull_pending && n.arrivals.empty() && n.st != I_PULL;
+    bool quiescent = n.interrupt_set.empty() && n.abort_set.empty() && !n.pull_pending && n.arrivals.empty() &&
+                     n.st != I_PULL;
     bool eq1 = n.pv == n.v && n.acc == (int)n.run.size() + (int)n.wait.size() + n.c;
     if (quiescent && !eq1) { s.m[M_VIOLATIONS]++; s.err = SFO_E_STATE; }
     if (!(quiescent && eq1)) valid = false;
@@ -616,7 +670,7 @@ void run_window(Scen &s) {
   // W6: commands to an idle instance apply now, as a boundary at t.
   for (int i = 0; i < s.I; ++i) {
     Inst &n = s.inst[i];
-    if (n.st == I_IDLE && (n.pull_pending || !n.interrupt_set.empty())) n.cmd_at_t = true;
+    if (n.st == I_IDLE && (n.pull_pending || !n.interrupt_set.empty() || !n.abort_set.empty())) n.cmd_at_t = true;
   }
   // W7: every instance advances through its boundaries <= t + Delta.
   for (int i = 0; i < s.I; ++i) {
@@ -665,7 +719,9 @@ int sfo_create(int32_t instances, int32_t eta, int32_t group_size, const sfo_con
     s.eta = cfg->scenario_eta ? cfg->scenario_eta[k] : eta;
     s.strategy = cfg->scenario_strategy ? cfg->scenario_strategy[k] : cfg->strategy;
     if (s.I < 1 || s.eta < 0) { delete sim; return SFO_E_INVALID; }
-    s.B = cfg->batch_size; s.G = group_size;
+    if (cfg->extra_groups < 0 || cfg->extra_members < 0) { delete sim; return SFO_E_INVALID; }
+    s.Br = cfg->batch_size; s.Gr = group_size;
+    s.B = cfg->batch_size + cfg->extra_groups; s.G = group_size + cfg->extra_members;
     s.P = Params{cfg->k1, cfg->k2, cfg->k3, cfg->k4, cfg->k5, cfg->kp, cfg->M,
                  cfg->mu, cfg->phi_tp, cfg->phi_wait, s.eta};
     s.delta = cfg->delta; s.r = cfg->r; s.q = cfg->q; s.R = cfg->R; s.atw = cfg->atw;
@@ -673,7 +729,7 @@ int sfo_create(int32_t instances, int32_t eta, int32_t group_size, const sfo_con
     s.traj.assign((size_t)s.pool_cap * s.G, Traj());
     s.grp.assign(s.pool_cap, Group());
     s.inst.assign(s.I, Inst());
-    s.L.eta = s.eta; s.L.B = s.B;
+    s.L.eta = s.eta; s.L.B = s.B; s.L.Br = s.Br;
     std::memset(s.m, 0, sizeof(s.m));
   }
   *out = sim;
@@ -738,8 +794,8 @@ int sfo_collect_batch(sfo_sim *sim, int32_t k, int32_t cap, int32_t *v_buf, int3
   if (!sim || k < 0 || k >= (int)sim->sc.size()) return SFO_E_RANGE;
   Scen &s = sim->sc[k];
   if (s.err) return SFO_E_STATE;
-  if (n_out) *n_out = s.B;
-  if (cap < s.B) return SFO_E_RANGE;
+  if (n_out) *n_out = s.Br;
+  if (cap < s.Br) return SFO_E_RANGE;
   if (s.L.state(s.L.cu) != 1) return SFO_NOT_READY;
   consume(s, v_buf, gids, gv);
   return s.err ? SFO_E_STATE : SFO_OK;
@@ -820,10 +876,11 @@ int sfo_dump_instances(sfo_sim *sim, int32_t k, int64_t *out, int64_t cap, int64
 }
 
 // ---------------------------------------------------------------- unit-level
-sfo_ledger *sfo_ledger_new(int32_t eta, int32_t B) {
-  if (eta < 0 || B < 1) return nullptr;
+sfo_ledger *sfo_ledger_new(int32_t eta, int32_t B) { return sfo_ledger_new2(eta, B, B); }
+sfo_ledger *sfo_ledger_new2(int32_t eta, int32_t cap, int32_t B) {
+  if (eta < 0 || B < 1 || cap < B) return nullptr;
   sfo_ledger *L = new (std::nothrow) sfo_ledger();
-  if (L) { L->eta = eta; L->B = B; }
+  if (L) { L->eta = eta; L->B = cap; L->Br = B; }
   return L;
 }
 void sfo_ledger_free(sfo_ledger *L) { delete L; }
@@ -849,8 +906,18 @@ int sfo_ledger_occupy(sfo_ledger *L, int32_t g, int32_t v, int32_t *b, int32_t *
 }
 int sfo_ledger_state(const sfo_ledger *L, int32_t b) { return L->state(b); }
 int sfo_ledger_consume(sfo_ledger *L, int32_t *groups, int32_t *versions) {
+  return sfo_ledger_consume2(L, groups, versions, nullptr, nullptr);
+}
+int sfo_ledger_consume2(sfo_ledger *L, int32_t *groups, int32_t *versions, int32_t *surplus, int32_t *n_surplus) {
   if (L->state(L->cu) != 1) return SFO_NOT_READY;
-  for (int s = 0; s < L->B; ++s) { groups[s] = L->buf[L->cu][s].g; versions[s] = L->buf[L->cu][s].v; }
+  int taken = 0, ns = 0;
+  for (int s = 0; s < L->B; ++s) {
+    const Entry &e = L->buf[L->cu][s];
+    if (e.st == E_EMPTY) continue;
+    if (e.st == E_OCCUPIED && taken < L->Br) { groups[taken] = e.g; versions[taken] = e.v; ++taken; }
+    else if (surplus) surplus[ns++] = e.g;
+  }
+  if (n_surplus) *n_surplus = ns;
   L->cu += 1;
   return SFO_OK;
 }

@@ -41,6 +41,8 @@ typedef struct {
   uint32_t strategy;                  /* bit0 R, bit1 S, bit2 M (1 = StaleFlow) */
   int32_t atw;                        /* auto-train windows; 0 = external trainer */
   int32_t pool_capacity_groups;       /* max groups submitted per scenario */
+  int32_t extra_groups;               /* batch-level redundancy: buffer slots = B + extra_groups (App C) */
+  int32_t extra_members;              /* group-level redundancy: members per group = G + extra_members  */
 } sfo_config;
 
 typedef struct sfo_sim sfo_sim;
@@ -70,13 +72,18 @@ int sfo_dump_instances(sfo_sim *, int32_t scenario, int64_t *out, int64_t cap, i
 /* ---------------- unit-level entry points (used by the oracle's own pins) ---------------- */
 typedef struct sfo_ledger sfo_ledger;
 sfo_ledger *sfo_ledger_new(int32_t eta, int32_t batch_size);
+/* batch-level redundancy: `capacity` slots per buffer, Ready at >= batch_size Occupied */
+sfo_ledger *sfo_ledger_new2(int32_t eta, int32_t capacity, int32_t batch_size);
 void sfo_ledger_free(sfo_ledger *);
 int sfo_ledger_verify(const sfo_ledger *, int32_t v);                           /* 1/0 */
 int sfo_ledger_reserve(sfo_ledger *, int32_t g, int32_t v, int32_t *b, int32_t *s);
 int sfo_ledger_delete_relocate(sfo_ledger *, int32_t g);
 int sfo_ledger_occupy(sfo_ledger *, int32_t g, int32_t v, int32_t *b, int32_t *s);
 int sfo_ledger_state(const sfo_ledger *, int32_t b);  /* 0 Waiting, 1 Ready, 2 Stuck */
+/* first batch_size Occupied entries in slot order; returns the surplus (aborted) groups through
+ * surplus[capacity] / *n_surplus when non-NULL */
 int sfo_ledger_consume(sfo_ledger *, int32_t *groups, int32_t *versions);
+int sfo_ledger_consume2(sfo_ledger *, int32_t *groups, int32_t *versions, int32_t *surplus, int32_t *n_surplus);
 int sfo_ledger_get(const sfo_ledger *, int32_t b, int32_t s, int32_t *st, int32_t *g, int32_t *v);
 int32_t sfo_ledger_cu(const sfo_ledger *);
 sfo_ledger *sfo_ledger_clone(const sfo_ledger *);
