@@ -519,8 +519,12 @@ void boundary(Scen &s, int i, int64_t b) {
     }
     n.interrupt_set.clear();
   }
-  // B1 (Abort): removed like an interrupt, but the trajectory does not return to the TS.
-  if (n.st != I_PULL && !n.abort_set.empty()) {
+  // B1 (Abort): removed like an interrupt, but the trajectory does not return to the TS.  Unlike
+  // interrupts (issued only on a valid snapshot, never to a pulling instance), aborts come from
+  // Consume and reward processing at any time, so they apply at every boundary, the end of a
+  // pull included (reading R-ABORT; a pulling instance was drained by Alg 3, so there only held
+  // arrivals can be aborted, and those are dropped at B6).
+  if (!n.abort_set.empty()) {
     for (int j : n.abort_set) {
       auto it = std::find(n.run.begin(), n.run.end(), j);
       if (it != n.run.end()) { n.kv -= (int64_t)P.k5 * ctx_len(s, j); n.run.erase(it); continue; }

@@ -52,10 +52,10 @@ def test_batch_level_ready_before_full():
     assert L.state(0) == "Ready"
 
 
-def small(B, G, eb=0, em=0, eta=1, I=2, steps=3, seed=0, strategy=7, M=1 << 20):
+def small(B, G, eb=0, em=0, eta=1, I=2, steps=3, seed=0, strategy=7, M=1 << 20, q=30):
     rng = random.Random(seed)
     cfg = Config(batch_size=B, n_scenarios=1, k1=1, k2=100, k3=10, k4=50, k5=1, kp=0, M=M, mu=0.3, phi_tp=5.0,
-                 phi_wait=3, delta=1000, r=5, q=30, R=20, strategy=strategy, atw=1, pool_capacity_groups=64,
+                 phi_wait=3, delta=1000, r=5, q=q, R=20, strategy=strategy, atw=1, pool_capacity_groups=64,
                  extra_groups=eb, extra_members=em)
     n_groups = (B + eb) * (steps + eta + 2)
     prompt = np.array([rng.randint(1, 40) for _ in range(n_groups)], np.int32)
@@ -104,14 +104,17 @@ def test_batch_level_surplus_groups_aborted():
         assert (lc[lc[:, 1] == g][:, 6] == CONSUMED).all()
 
 
-@pytest.mark.parametrize("seed", range(30))
+@pytest.mark.parametrize("seed", range(60))
 def test_redundancy_fuzz_invariants(seed):
+    """Seeds 30+ use long pulls (q = 1500 ps > Delta) so that aborts land on pulling instances
+    (reading R-ABORT: removal at the end of the pull)."""
     rng = random.Random(7000 + seed)
     B, G = rng.randint(1, 5), rng.randint(1, 4)
     eb, em, eta = rng.randint(0, 2), rng.randint(0, 2), rng.randint(0, 3)
     steps = rng.randint(2, 4)
     s, n_groups = small(B, G, eb, em, eta, I=rng.randint(1, 3), steps=steps, seed=seed,
-                        strategy=rng.randint(0, 7), M=rng.choice([200, 500, 1 << 20]))
+                        strategy=rng.randint(0, 7), M=rng.choice([200, 500, 1 << 20]),
+                        q=30 if seed < 30 else 1500)
     run_batches(s, steps)
     m = s.metrics()
     assert m[IDX["violations"]] == 0
