@@ -65,6 +65,15 @@ typedef struct {
   int32_t pool_capacity_groups;       /* max groups ever submitted per scenario (device pool)    */
   int32_t command_log_capacity;       /* per-scenario command records kept for sf_dump_commands  */
                                       /*   (0 = keep only the command hash)                      */
+  int32_t extra_groups;               /* batch-level redundant rollout (App C):    */
+                                      /*   buffers hold batch_size + extra_groups slots, are     */
+                                      /*   Ready at >= batch_size Occupied; Consume returns the  */
+                                      /*   first batch_size Occupied (slot order) and Aborts the */
+                                      /*   surplus groups.  0 = off                  */
+  int32_t extra_members;              /* group-level redundancy: group_size + extra_members      */
+                                      /*   members are rolled out per group; a group completes   */
+                                      /*   at group_size rewarded members and its other members  */
+                                      /*   are Aborted at once (P:473 footnote)      */
   int32_t device;                     /* CUDA device ordinal                                     */
   void *cuda_stream;                  /* cudaStream_t (e.g. torch.cuda.Stream().cuda_stream)     */
 } sf_config;
@@ -84,8 +93,8 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
 void sf_destroy(sf_ctx *ctx);
 
 /* Append n_groups prompts to a scenario's dataset pool: prompt_len[n_groups] and
- * target_len[n_groups*group_size] (the simulated response length of each member).  Host
- * pointers, copied.  Ingestion into the TS happens inside sf_step under the (eta+1)*B
+ * target_len[n_groups*(group_size+extra_members)] (the simulated response length of each
+ * member, the redundant ones included).  Host pointers, copied.  Ingestion into the TS happens inside sf_step under the (eta+1)*B
  * live-group cap.  Errors: SF_E_RANGE (scenario, pool capacity), SF_E_INVALID (target < 1 or
  * k5*(prompt+target) > M, reading A27). */
 sf_status sf_submit_prompts(sf_ctx *ctx, int32_t scenario, int32_t n_groups, const int32_t *prompt_len,
@@ -107,7 +116,8 @@ sf_status sf_step(sf_ctx *ctx, int32_t n_windows, sf_step_stats *out);
 sf_status sf_publish_params(sf_ctx *ctx, int32_t scenario, int32_t new_version);
 
 /* External-trainer Consume: if the earliest unconsumed buffer is Ready, write its
- * v_buf, the B group ids in slot order and their versions, set *n_out = B and retire it.
+ * v_buf, the B group ids in slot order and their versions, set *n_out = B and retire it
+ * (with extra_groups > 0: the first B Occupied entries; the surplus groups are Aborted).
  * SF_NOT_READY if Waiting/Stuck; SF_E_RANGE if cap < B (*n_out = B). */
 sf_status sf_collect_batch(sf_ctx *ctx, int32_t scenario, int32_t cap, int32_t *v_buf, int32_t *group_ids,
                            int32_t *group_versions, int32_t *n_out);
@@ -125,12 +135,12 @@ sf_status sf_read_scenario_metrics(sf_ctx *ctx, int32_t scenario, int64_t *out, 
 sf_status sf_read_all_scenario_metrics(sf_ctx *ctx, int64_t *out, int64_t cap);
 
 /* Per-trajectory lifecycle records, 13 int64 each: id, group, prompt, target, gen, v_group,
- * state (0 pool,1 TS,2 transit,3 wait,4 run,5 done,6 consumed), inst, n_routes, n_preempt,
+ * state (0 pool,1 TS,2 transit,3 wait,4 run,5 done,6 consumed,7 aborted), inst, n_routes, n_preempt,
  * n_interrupt, consumed_vbuf, t_complete.  *n = records available. */
 sf_status sf_dump_lifecycles(sf_ctx *ctx, int32_t scenario, int64_t *records, int64_t cap, int64_t *n);
 /* Consumed batches: per batch v_buf then B (group id, group version) pairs (int32). */
 sf_status sf_dump_batches(sf_ctx *ctx, int32_t scenario, int32_t *out, int64_t cap, int64_t *n);
-/* Command log (4 int64 per record: window, kind 1 Route/2 Interrupt/3 Pull, inst, traj);
+/* Command log (4 int64 per record: window, kind 1 Route/2 Interrupt/3 Pull/4 Abort, inst, traj);
  * records beyond command_log_capacity are dropped (the hash in the metrics covers all). */
 sf_status sf_dump_commands(sf_ctx *ctx, int32_t scenario, int64_t *records, int64_t cap, int64_t *n);
 /* Per-instance view, 7 int64 each: v, kv, n_run, n_wait, complete, state(0 idle,1 tick,2 pull),

@@ -23,6 +23,7 @@ constexpr int kWarpsPerBlock = 8;
 
 struct InstState {
   int st, pullv, pullpend, intkind, intk, cc, v, run_n, whead, wn, arr_n, arr_head;
+  int abortn, abortarr;                     // pending Aborts: run/wait members, undelivered arrivals
   long long nb, until, kv, prefill, t_cmd;
   long long ticks, iters, tokens, comps, preempts;
 };
@@ -37,6 +38,34 @@ __device__ __forceinline__ void emit_completion(const GParams &P, const Dev &D, 
   D.t_complete[j] = b;                      // reward due at b + R
   const int e = atomicAdd(&SS.ev_n, 1);
   D.ev_id[C.ev_off + e] = id;
+}
+
+// B1 (Abort, reading R-ABORT): drop the aborted members from the wait ring, FIFO order kept
+// (in-place forward compaction, 32 entries per step).  Returns the new queue length.
+__device__ __forceinline__ int compact_wait_aborted(const Dev &D, const ScenConst &C, long long lb, int whead, int wn) {
+  const int cap = C.cap;
+  int out = 0;
+  for (int k0 = 0; k0 < wn; k0 += 32) {
+    const int k = k0 + (int)lane_id();
+    int id = 0;
+    bool keep = false;
+    if (k < wn) {
+      int pos = whead + k;
+      if (pos >= cap) pos -= cap;
+      id = D.wait_id[lb + pos];
+      keep = D.loc[C.traj_off + id] != L_ABORTED;
+    }
+    const unsigned km = __ballot_sync(0xffffffffu, keep);
+    __syncwarp();
+    if (keep) {
+      int pos = whead + out + __popc(km & lanemask_lt());
+      if (pos >= cap) pos -= cap;
+      D.wait_id[lb + pos] = id;
+    }
+    out += __popc(km);
+    __syncwarp();
+  }
+  return out;
 }
 
 // ------------------------------------------------------------------ register-resident path
@@ -145,6 +174,33 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
       blocked = false;
       x.intkind = INT_NONE;
     }
+    // B1 (Abort): aborted run / wait members leave for good, their KV released (reading R-ABORT)
+    if (x.abortn > 0) {
+      long long release = 0;
+      int nab = 0;
+#pragma unroll
+      for (int q = 0; q < kR; ++q) {
+        const bool a = ((live[q] >> lane) & 1u) && D.loc[C.traj_off + rid[q]] == L_ABORTED;
+        const unsigned am = __ballot_sync(0xffffffffu, a);
+        if (a) { release += k5 * (long long)(fin[q] - rem[q]); rem[q] = kDead; }   // p + gen
+        live[q] &= ~am;
+        nab += __popc(am);
+      }
+      if (nab) {
+        x.kv -= warp_sum(release);
+        nlive -= nab;
+        int t = 0;
+#pragma unroll
+        for (int q = 0; q < kR; ++q)
+          if (live[q]) t = q * 32 + 32 - __clz(live[q]);
+        tail = t;
+      }
+      x.wn = compact_wait_aborted(D, C, lb, x.whead, x.wn);
+      x.abortn = 0;
+      head_ok = false;
+      blocked = false;
+      arr_ring0 = -1;                                  // ring positions moved: stop mapping arrivals
+    }
     if (tick_end) {
       // B2 + B3 in registers: one token per running trajectory, ballot the completions
       const int n0 = nlive;
@@ -252,11 +308,16 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
       do {
         if (x.arr_head >= b6 + 32) load6(x.arr_head);
         const int id = __shfl_sync(0xffffffffu, a6_id, x.arr_head - b6);
-        int pos = x.whead + x.wn;
-        if (pos >= cap) pos -= cap;
-        if (x.arr_head == 0) arr_ring0 = pos;
-        if (lane == 0) { D.wait_id[lb + pos] = id; D.loc[C.traj_off + id] = L_WAIT; }
-        ++x.wn;
+        if (x.abortarr > 0 && D.loc[C.traj_off + id] == L_ABORTED) {   // aborted in transit: dropped
+          --x.abortarr;
+          arr_ring0 = -1;
+        } else {
+          int pos = x.whead + x.wn;
+          if (pos >= cap) pos -= cap;
+          if (x.arr_head == 0) arr_ring0 = pos;
+          if (lane == 0) { D.wait_id[lb + pos] = id; D.loc[C.traj_off + id] = L_WAIT; }
+          ++x.wn;
+        }
         ++x.arr_head;
         next_arr = arr_time(x.arr_head);
       } while (next_arr <= b);
@@ -442,6 +503,30 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
       else x.wn -= x.intk;
       x.intkind = INT_NONE;
     }
+    if (x.abortn > 0) {                              // B1 (Abort), reading R-ABORT
+      int out = 0;
+      long long release = 0;
+      for (int base = 0; base < x.run_n; base += 32) {
+        const int k = base + (int)lane;
+        int rem = 0, id = 0;
+        bool ab = false;
+        if (k < x.run_n) {
+          rem = D.run_rem[lb + k]; id = D.run_id[lb + k];
+          ab = D.loc[C.traj_off + id] == L_ABORTED;
+          if (ab) release += k5 * (long long)(D.prompt[C.grp_off + grp_of(P, id)] + D.T[C.traj_off + id] - rem);
+        }
+        const bool keep = k < x.run_n && !ab;
+        const unsigned mk = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();
+        if (keep) { const int pos = out + __popc(mk & lanemask_lt()); D.run_rem[lb + pos] = rem; D.run_id[lb + pos] = id; }
+        out += __popc(mk);
+        __syncwarp();
+      }
+      x.kv -= warp_sum(release);
+      x.run_n = out;
+      x.wn = compact_wait_aborted(D, C, lb, x.whead, x.wn);
+      x.abortn = 0;
+    }
     if (tick_end) {
       const int n0 = x.run_n;
       int out = 0, ncomp = 0;
@@ -498,6 +583,11 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
     }
     while (x.arr_head < x.arr_n && D.arr_t[lb + x.arr_head] <= b) {
       const int id = D.arr_id[lb + x.arr_head];
+      if (x.abortarr > 0 && D.loc[C.traj_off + id] == L_ABORTED) {   // aborted in transit: dropped
+        --x.abortarr;
+        ++x.arr_head;
+        continue;
+      }
       int pos = x.whead + x.wn;
       if (pos >= cap) pos -= cap;
       if (lane == 0) { D.wait_id[lb + pos] = id; D.loc[C.traj_off + id] = L_WAIT; }
@@ -556,9 +646,10 @@ __device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D,
   x.kv = D.ikv[gi]; x.prefill = D.iprefill[gi]; x.cc = D.ic[gi]; x.v = D.iv[gi];
   x.run_n = D.irun_n[gi]; x.whead = D.iwhead[gi]; x.wn = D.iwn[gi];
   x.arr_n = D.iarr_n[gi]; x.arr_head = 0;
+  x.abortn = D.iabort[gi]; x.abortarr = D.iabort_arr[gi];
   x.ticks = x.iters = x.tokens = x.comps = x.preempts = 0;
   // W6: commands to an idle instance apply at a boundary at t
-  x.t_cmd = (x.st == I_IDLE && (x.pullpend || x.intkind != INT_NONE)) ? t : kInf;
+  x.t_cmd = (x.st == I_IDLE && (x.pullpend || x.intkind != INT_NONE || x.abortn > 0)) ? t : kInf;
 
   if (x.run_n + x.wn + x.arr_n <= 32 * kR) advance_reg(P, D, C, SS, x, lb, t_end, stage);
   else advance_global(P, D, C, SS, x, lb, t_end);
@@ -581,6 +672,8 @@ __device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D,
     D.ipullpend[gi] = x.pullpend; D.iintkind[gi] = x.intkind;
     D.ikv[gi] = x.kv; D.iprefill[gi] = x.prefill; D.ic[gi] = x.cc; D.iv[gi] = x.v;
     D.irun_n[gi] = x.run_n; D.iwhead[gi] = x.whead; D.iwn[gi] = x.wn; D.iarr_n[gi] = remain;
+    if (x.abortn != D.iabort[gi]) D.iabort[gi] = x.abortn;
+    if (x.abortarr != D.iabort_arr[gi]) D.iabort_arr[gi] = x.abortarr;
     metric_add(SS, M_TICKS, x.ticks);
     metric_add(SS, M_TRAJ_ITERS, x.iters);
     metric_add(SS, M_TOKENS, x.tokens);

@@ -608,7 +608,7 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
   int live = SS.live, err = 0;
   int dbg_tent = 0;
   long long m_pub = 0, m_batches = 0, m_ingested = 0, m_valid = 0, m_invalid = 0, m_viol = 0;
-  long long m_routes = 0, m_interrupts = 0, m_pulls = 0, m_reserves = 0;
+  long long m_routes = 0, m_interrupts = 0, m_pulls = 0, m_reserves = 0, m_aborts = 0;
   const int nring = C.eta + 1;
 
   // ---------------- W0: auto trainer (reading A24): publish if due, then Consume if Ready
@@ -620,33 +620,19 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
       busy = 0;
     }
     const int ring = c.cu % nring;
-    if (!busy && D.led_nocc[C.ring_off + ring] == P.B) {
-      const long long base = C.led_off + (long long)ring * P.B;
-      const long long bl = C.batch_off + (long long)SS.batch_n * (1 + 2 * P.B);
-      if (lane == 0) D.batches[bl] = c.cu;
-      for (int k = lane; k < P.B; k += 32) {
-        const int g = D.led_g[base + k], v = D.led_v[base + k];
-        D.batches[bl + 1 + 2 * k] = g;
-        D.batches[bl + 2 + 2 * k] = v;
-        const int stal = c.cu - v;                 // staleness V_buf - V_traj (A30)
-        if (stal < 0 || stal > C.eta) { atomicAdd(&SS.m[M_VIOLATIONS], 1ULL); err = ERR_STALENESS; }
-        atomicAdd(&SS.m[M_HIST0 + min(max(stal, 0), 8)], 1ULL);
-        D.cvbuf[C.grp_off + g] = c.cu;
-        for (int m = 0; m < P.G; ++m) D.loc[C.traj_off + (long long)g * P.G + m] = L_CONSUMED;
-        D.led_st[base + k] = E_EMPTY;
-        D.led_g[base + k] = -1;
-        D.led_v[base + k] = -1;
-      }
-      __syncwarp();
+    if (!busy && D.led_nocc[C.ring_off + ring] >= P.Br) {      // Ready (App C: >= B Occupied)
+      CmdLog cl{c.hash, c.cmd_n, c.window, 0};
+      const int retired = consume_buffer(P, D, C, SS, ring, c.cu, cl, err, nullptr);
+      c.hash = cl.hash; c.cmd_n = cl.cmd_n; m_aborts = cl.aborts;
       if (lane == 0) {
         D.led_nocc[C.ring_off + ring] = 0;
         D.led_nres[C.ring_off + ring] = 0;
         SS.batch_n += 1;
         SS.publish_at = c.t + (long long)P.atw * P.delta;
       }
+      live -= retired;
       busy = 1;
       c.cu += 1;
-      live -= P.B;
       m_batches = 1;
     }
     __syncwarp();
@@ -656,7 +642,7 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
   // oldest live group (bounds the TS bitmap scan): skip consumed groups
   for (;;) {
     const int g = c.min_live_g + (int)lane;
-    const bool consumed = g < c.n_ingested && D.cvbuf[C.grp_off + g] >= 0;
+    const bool consumed = g < c.n_ingested && D.cvbuf[C.grp_off + g] != -1;   // consumed or aborted
     const unsigned m = __ballot_sync(0xffffffffu, !consumed);
     if (m) { c.min_live_g += __ffs(m) - 1; break; }
     c.min_live_g += 32;
@@ -679,7 +665,8 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
   bool ok = true;
   for (int i = lane; i < C.I; i += 32) {
     const long long gi = C.inst_off + i;
-    const bool quiescent = D.iintkind[gi] == INT_NONE && !D.ipullpend[gi] && D.iarr_n[gi] == 0 && D.ist[gi] != I_PULL;
+    const bool quiescent = D.iintkind[gi] == INT_NONE && !D.ipullpend[gi] && D.iarr_n[gi] == 0 && D.ist[gi] != I_PULL &&
+                           D.iabort[gi] == 0;
     const bool eq1 = D.ipv[gi] == D.iv[gi] && D.iacc[gi] == D.irun_n[gi] + D.iwn[gi] + D.ic[gi];
     if (quiescent && !eq1) err = ERR_EQ1;
     ok &= quiescent && eq1;
@@ -923,6 +910,7 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
     metric_add(SS, M_INTERRUPTS, m_interrupts);
     metric_add(SS, M_PULLS, m_pulls);
     metric_add(SS, M_RESERVES, m_reserves);
+    metric_add(SS, M_ABORTS, m_aborts);
 #ifdef SF_TIMING
     if (D.dbg) {
       D.dbg[8 * s + 0] = clock64() - t0_clk;

@@ -12,36 +12,29 @@ __global__ void __launch_bounds__(128) k_ledger(GParams P, Dev D) {
 }
 
 // External-trainer Consume for one scenario; out[0] = status (0 ok, 1 not ready),
-// out[1] = v_buf, then B (group, version) pairs.
+// out[1] = v_buf, then Br (group, version) pairs (surplus groups Aborted, consume_buffer).
 __global__ void k_collect(GParams P, Dev D, int s, int *out) {
   const unsigned lane = lane_id();
   const ScenConst C = D.sc[s];
   ScenState &SS = D.ss[s];
   const int cu = SS.cu;
   const int ring = cu % (C.eta + 1);
-  if (D.led_nocc[C.ring_off + ring] != P.B) { if (lane == 0) out[0] = 1; return; }
-  const long long base = C.led_off + (long long)ring * P.B;
-  const long long bl = C.batch_off + (long long)SS.batch_n * (1 + 2 * P.B);
-  if (lane == 0) { out[0] = 0; out[1] = cu; D.batches[bl] = cu; }
-  for (int k = lane; k < P.B; k += 32) {
-    const int g = D.led_g[base + k], v = D.led_v[base + k];
-    out[2 + 2 * k] = g; out[3 + 2 * k] = v;
-    D.batches[bl + 1 + 2 * k] = g; D.batches[bl + 2 + 2 * k] = v;
-    const int stal = cu - v;
-    if (stal < 0 || stal > C.eta) { atomicAdd(&SS.m[M_VIOLATIONS], 1ULL); SS.err = ERR_STALENESS; }
-    atomicAdd(&SS.m[M_HIST0 + min(max(stal, 0), 8)], 1ULL);
-    D.cvbuf[C.grp_off + g] = cu;
-    for (int m = 0; m < P.G; ++m) D.loc[C.traj_off + (long long)g * P.G + m] = L_CONSUMED;
-    D.led_st[base + k] = E_EMPTY; D.led_g[base + k] = -1; D.led_v[base + k] = -1;
-  }
-  __syncwarp();
+  if (D.led_nocc[C.ring_off + ring] < P.Br) { if (lane == 0) out[0] = 1; return; }
+  if (lane == 0) { out[0] = 0; out[1] = cu; }
+  CmdLog cl{SS.cmd_hash, SS.cmd_n, SS.window, 0};
+  int err = 0;
+  const int retired = consume_buffer(P, D, C, SS, ring, cu, cl, err, out + 2);
+  err = warp_max(err);
   if (lane == 0) {
     D.led_nocc[C.ring_off + ring] = 0;
     D.led_nres[C.ring_off + ring] = 0;
     SS.batch_n += 1;
     SS.cu = cu + 1;
-    SS.live -= P.B;
+    SS.live -= retired;
+    SS.cmd_hash = cl.hash; SS.cmd_n = cl.cmd_n;
     SS.m[M_BATCHES] += 1;
+    SS.m[M_ABORTS] += cl.aborts;
+    if (err) SS.err = err;
   }
 }
 
@@ -72,8 +65,8 @@ __global__ void k_dump_lifecycles(GParams P, Dev D, int s, long long n_traj, lon
     const int g = (int)(j / P.G);
     long long *r = out + 13 * j;
     r[0] = j; r[1] = g; r[2] = D.prompt[C.grp_off + g]; r[3] = D.T[a]; r[4] = D.gen[a];
-    r[5] = D.gv[C.grp_off + g]; r[6] = D.loc[a]; r[7] = D.tinst[a]; r[8] = D.n_routes[a];
-    r[9] = D.n_preempt[a]; r[10] = D.n_interrupt[a]; r[11] = D.cvbuf[C.grp_off + g]; r[12] = D.t_complete[a];
+    r[5] = D.gv[C.grp_off + g]; r[6] = D.loc[a] == L_REWARDED ? L_DONE : D.loc[a]; r[7] = D.tinst[a]; r[8] = D.n_routes[a];
+    r[9] = D.n_preempt[a]; r[10] = D.n_interrupt[a]; r[11] = max(D.cvbuf[C.grp_off + g], -1); r[12] = D.t_complete[a];
   }
 }
 // running trajectories: gen = T - rem from the run lists

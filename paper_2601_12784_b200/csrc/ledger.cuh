@@ -120,6 +120,7 @@ __device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, 
   const int cu = SS.cu;
   int err = 0;
   long long m_reloc = 0, m_occ = 0;
+  CmdLog cl{SS.cmd_hash, SS.cmd_n, SS.window, 0};
   int np = 0;
   if (n <= kEvStage) {
     // stage (t_complete, id), rank-sort by (t_reward, id) (W8) in shared memory
@@ -147,16 +148,24 @@ __device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, 
       const bool ok = valid && es.t[e] + P.R <= t_end;
       const int g = grp_of(P, id);
       const unsigned okm = __ballot_sync(0xffffffffu, ok);
-      const int nrw = ok ? D.n_rew[C.grp_off + g] : 0;
-      const unsigned same = __match_any_sync(0xffffffffu, ok ? g : -1 - (int)lane);
+      // redundancy: the reward of an aborted member is ignored, and inside this batch the
+      // members of a group past its Gr-th reward are aborted when the group completes
+      bool eff = ok;
+      if (P.red && ok) eff = D.loc[C.traj_off + id] != L_ABORTED;
+      const int nrw = eff ? D.n_rew[C.grp_off + g] : 0;
+      const unsigned same = __match_any_sync(0xffffffffu, eff ? g : -1 - (int)lane);
       const int nr = nrw + 1 + __popc(same & lanemask_lt());
-      if (ok && (same >> lane) == 1u) D.n_rew[C.grp_off + g] = nrw + __popc(same);   // last of its group
-      unsigned cm = __ballot_sync(0xffffffffu, ok && nr == P.G);
+      if (eff && (same >> lane) == 1u) D.n_rew[C.grp_off + g] = min(nrw + __popc(same), P.Gr);   // last of its group
+      if (P.red && eff && nr <= P.Gr) D.loc[C.traj_off + id] = L_REWARDED;
+      unsigned cm = __ballot_sync(0xffffffffu, eff && nr == P.Gr);
       __syncwarp();
       while (cm) {
         const int l = __ffs(cm) - 1;
         cm &= cm - 1;
-        complete_group(P, D, C, SS, __shfl_sync(0xffffffffu, g, l), cu, m_reloc, m_occ, err);
+        const int gc = __shfl_sync(0xffffffffu, g, l);
+        if (P.red)                                      // group-level redundancy: Abort the others
+          for (int m = 0; m < P.G; ++m) abort_member(P, D, C, cl, gc * P.G + m);
+        complete_group(P, D, C, SS, gc, cu, m_reloc, m_occ, err);
         if (err) break;
       }
       np += __popc(okm);
@@ -182,11 +191,17 @@ __device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, 
       const int id = tmp[np];
       if (D.t_complete[C.traj_off + id] + P.R > t_end) break;
       const int g = grp_of(P, id);
+      if (P.red && D.loc[C.traj_off + id] == L_ABORTED) continue;     // ignored reward
       const int nr = D.n_rew[C.grp_off + g] + 1;
       __syncwarp();
-      if (lane == 0) D.n_rew[C.grp_off + g] = nr;
+      if (lane == 0) {
+        D.n_rew[C.grp_off + g] = nr;
+        if (P.red) D.loc[C.traj_off + id] = L_REWARDED;
+      }
       __syncwarp();
-      if (nr == P.G) {
+      if (nr == P.Gr) {
+        if (P.red)
+          for (int m = 0; m < P.G; ++m) abort_member(P, D, C, cl, g * P.G + m);
         complete_group(P, D, C, SS, g, cu, m_reloc, m_occ, err);
         if (err) break;
       }
@@ -196,12 +211,14 @@ __device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, 
   __syncwarp();
   if (lane == 0) {
     SS.ev_n = n - np;
+    SS.cmd_hash = cl.hash; SS.cmd_n = cl.cmd_n;
     SS.t = t_end;                                       // W9
     SS.window += 1;
     if (err) SS.err = err;
     metric_add(SS, M_WINDOWS, 1);
     metric_add(SS, M_RELOCATIONS, m_reloc);
     metric_add(SS, M_OCCUPIED, m_occ);
+    metric_add(SS, M_ABORTS, cl.aborts);
   }
 }
 

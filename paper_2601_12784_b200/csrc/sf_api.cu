@@ -152,7 +152,8 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
   if (!cfg || !out || group_size < 1 || group_size > 4096 || cfg->batch_size < 1 || cfg->n_scenarios < 1 || cfg->k5_tok < 1 ||
       cfg->snap_period_ps <= 0 || cfg->pool_capacity_groups < 1 || cfg->kv_budget_tok < 1 ||
       cfg->command_log_capacity < 0 || cfg->route_lat_ps < 0 || cfg->pull_lat_ps < 0 || cfg->reward_lat_ps < 0 ||
-      cfg->auto_train_windows < 0)
+      cfg->auto_train_windows < 0 || cfg->extra_groups < 0 || cfg->extra_members < 0 ||
+      group_size + cfg->extra_members > 4096 || cfg->extra_groups > (1 << 20))
     return SF_E_INVALID;
   // 32-bit products on the hot path (sf_internal.cuh tick_latency): k1, k3, kp, k5 < 2^31, M < 2^30
   if (cfg->k1_ps_per_tok < 0 || cfg->k1_ps_per_tok >= (1LL << 31) || cfg->k3_ps < 0 || cfg->k3_ps >= (1LL << 31) ||
@@ -167,9 +168,13 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
   if (cudaSetDevice(cfg->device) != cudaSuccess) { delete c; return SF_E_CUDA; }
   struct Restore { int d; ~Restore() { cudaSetDevice(d); } } restore{prev_dev};
   c->stream = (cudaStream_t)cfg->cuda_stream;
-  const int ns = cfg->n_scenarios, B = cfg->batch_size, G = group_size;
+  // redundant rollout (App C): B buffer slots and G members per group include the extra ones;
+  // Br groups form a batch and Gr rewarded members complete a group
+  const int ns = cfg->n_scenarios, B = cfg->batch_size + cfg->extra_groups, G = group_size + cfg->extra_members;
   GParams &P = c->P;
   P.B = B; P.G = G;
+  P.Br = cfg->batch_size; P.Gr = group_size;
+  P.red = P.Br < B || P.Gr < G;
   P.k1 = cfg->k1_ps_per_tok; P.k2 = cfg->k2_ps; P.k3 = cfg->k3_ps; P.k4 = cfg->k4_ps;
   P.k5 = cfg->k5_tok; P.kp = cfg->kprefill_ps_per_tok; P.M = cfg->kv_budget_tok;
   P.k1i = (int)P.k1; P.k3i = (int)P.k3; P.kpi = (int)P.kp;
@@ -184,7 +189,7 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
   long long inst = 0, led = 0, ring = 0, list = 0, bits = 0, mlq = 0, ev = 0, batch = 0, cmd = 0;
   const long long pool_traj = (long long)P.pool_cap * G;
   const long long bwords = (pool_traj + 31) / 32;
-  const long long batch_rec = (long long)(P.pool_cap / B + 1) * (1 + 2 * B);
+  const long long batch_rec = (long long)(P.pool_cap / P.Br + 1) * (1 + 2 * P.Br);
   for (int s = 0; s < ns; ++s) {
     ScenConst &S = c->hsc[s];
     S.I = cfg->scenario_instances ? cfg->scenario_instances[s] : instances;
@@ -231,14 +236,15 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
        dalloc(c, &D.iintk, inst, 0) && dalloc(c, &D.irun_n, inst, 0) && dalloc(c, &D.iwhead, inst, 0) &&
        dalloc(c, &D.iwn, inst, 0) && dalloc(c, &D.iarr_n, inst, 0) && dalloc(c, &D.ipv, inst, 0) &&
        dalloc(c, &D.iacc, inst, 0) && dalloc(c, &D.ikv, inst, 0) && dalloc(c, &D.inb, inst, 0) &&
-       dalloc(c, &D.iuntil, inst, 0) && dalloc(c, &D.iprefill, inst, 0);
+       dalloc(c, &D.iuntil, inst, 0) && dalloc(c, &D.iprefill, inst, 0) && dalloc(c, &D.iabort, inst, 0) &&
+       dalloc(c, &D.iabort_arr, inst, 0);
   ok = ok && dalloc(c, &D.run_id, list, 0) && dalloc(c, &D.run_rem, list, 0) && dalloc(c, &D.wait_id, list, 0) &&
        dalloc(c, &D.arr_id, list, 0) && dalloc(c, &D.arr_t, list, 0);
   ok = ok && dalloc(c, &D.led_st, led, 0) && dalloc(c, &D.led_g, led, 0xFF) && dalloc(c, &D.led_v, led, 0xFF) &&
        dalloc(c, &D.led_nres, ring, 0) && dalloc(c, &D.led_nocc, ring, 0);
   ok = ok && dalloc(c, &D.ev_t, 1, 0) && dalloc(c, &D.ev_id, ev, 0) && dalloc(c, &D.tsv_bits, bits, 0) &&
        dalloc(c, &D.mlq, mlq, 0) && dalloc(c, &D.batches, batch, 0) && dalloc(c, &D.cmdlog, cmd, 0);
-  ok = ok && dalloc(c, &c->d_metrics, sf::kMetrics, 0) && dalloc(c, &c->d_collect, 2 + 2 * B, 0);
+  ok = ok && dalloc(c, &c->d_metrics, sf::kMetrics, 0) && dalloc(c, &c->d_collect, 2 + 2 * P.Br, 0);
   if (!ok) {
     sf_destroy(c);
     return SF_E_NOMEM;
@@ -404,7 +410,7 @@ sf_status sf_collect_batch(sf_ctx *c, int32_t scenario, int32_t cap, int32_t *v_
   if (st != SF_OK) return st;
   DevGuard dg(c->device);
   if (scenario < 0 || scenario >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
-  const int B = c->P.B;
+  const int B = c->P.Br;
   if (n_out) *n_out = B;
   if (cap < B) return fail(c, SF_E_RANGE, "collect: cap < batch_size");
   sf_launch_collect(c->P, c->D, scenario, c->d_collect, c->stream);
@@ -520,7 +526,7 @@ sf_status sf_dump_batches(sf_ctx *c, int32_t scenario, int32_t *out, int64_t cap
   if (scenario < 0 || scenario >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
   ScenState s;
   if ((st = read_state(c, scenario, &s)) != SF_OK) return st;
-  const long long cnt = (long long)s.batch_n * (1 + 2 * c->P.B);
+  const long long cnt = (long long)s.batch_n * (1 + 2 * c->P.Br);
   if (n) *n = cnt;
   if (cap < cnt || (cnt > 0 && !out)) return SF_E_RANGE;
   if (cnt == 0) return SF_OK;

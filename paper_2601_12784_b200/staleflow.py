@@ -41,6 +41,7 @@ class SfConfig(C.Structure):
         ("snap_period_ps", C.c_int64), ("route_lat_ps", C.c_int64), ("pull_lat_ps", C.c_int64),
         ("reward_lat_ps", C.c_int64), ("strategy", C.c_uint32), ("auto_train_windows", C.c_int32),
         ("pool_capacity_groups", C.c_int32), ("command_log_capacity", C.c_int32),
+        ("extra_groups", C.c_int32), ("extra_members", C.c_int32),
         ("device", C.c_int32), ("cuda_stream", C.c_void_p),
     ]
 
@@ -118,7 +119,7 @@ class StaleFlow:
                  phi_wait: int = W.PHI_WAIT, snap_period: int = W.PS_PER_S, route_lat: int = 10_000_000_000,
                  pull_lat: int = 2 * W.PS_PER_S, reward_lat: int = W.PS_PER_S, strategy: int = W.STRAT_SF,
                  auto_train_windows: int = 0, pool_capacity_groups: int = 1024, command_log_capacity: int = 0,
-                 device: Optional[int] = None, stream=None):
+                 extra_groups: int = 0, extra_members: int = 0, device: Optional[int] = None, stream=None):
         import torch  # device + stream plumbing only
         if not torch.cuda.is_available():
             raise SfError("StaleFlow needs a CUDA device (no CPU fallback)")
@@ -126,6 +127,7 @@ class StaleFlow:
         if device is None:
             device = torch.cuda.current_device()
         self.G, self.B, self.n_scen = group_size, batch_size, n_scenarios
+        self.members = group_size + extra_members          # rolled out per group (App C)
         if stream is None:
             stream = torch.cuda.current_stream(device)
         self.stream = stream
@@ -147,7 +149,7 @@ class StaleFlow:
                        snap_period_ps=snap_period, route_lat_ps=route_lat, pull_lat_ps=pull_lat,
                        reward_lat_ps=reward_lat, strategy=strategy, auto_train_windows=auto_train_windows,
                        pool_capacity_groups=pool_capacity_groups, command_log_capacity=command_log_capacity,
-                       device=device, cuda_stream=C.c_void_p(stream.cuda_stream))
+                       extra_groups=extra_groups, extra_members=extra_members, device=device, cuda_stream=C.c_void_p(stream.cuda_stream))
         self.h = C.c_void_p()
         rc = self.L.sf_create(instances, eta, group_size, C.byref(cfg), C.byref(self.h))
         if rc != 0:
@@ -162,7 +164,8 @@ class StaleFlow:
                    kv_budget=p.kv_budget, mu=p.mu, phi_throughput=p.phi_tp, phi_wait=p.phi_wait,
                    snap_period=p.snap_period_ps, route_lat=p.route_lat_ps, pull_lat=p.pull_lat_ps,
                    reward_lat=p.reward_lat_ps, strategy=scs[0].strategy,
-                   auto_train_windows=p.auto_train_windows,
+                   auto_train_windows=p.auto_train_windows, extra_groups=p.extra_groups,
+                   extra_members=p.extra_members,
                    pool_capacity_groups=kw.pop("pool_capacity_groups", p.pool_groups), **kw)
 
     # ------------------------------------------------------------------ lifecycle

@@ -123,21 +123,29 @@ class Preset:
     mu: float = MU
     phi_wait: int = PHI_WAIT
     phi_tp: float = PHI_TP
+    extra_groups: int = 0                 # batch-level redundant rollout (App C)
+    extra_members: int = 0                # group-level redundant rollout (P:473 footnote)
+
+    @property
+    def members(self) -> int:
+        """Members rolled out per group, the redundant ones included."""
+        return self.group_size + self.extra_members
 
     @property
     def pool_groups(self) -> int:
-        """Groups submitted per scenario: enough for every train step plus the TS cap."""
+        """Groups submitted per scenario: enough for every train step plus the TS cap (a batch
+        retires up to batch_size + extra_groups groups)."""
         etamax = max(s.eta for s in self.scenarios)
-        return self.batch_size * (self.train_steps + etamax + 1)
+        return (self.batch_size + self.extra_groups) * (self.train_steps + etamax + 1)
 
     def max_inflight(self, eta: int) -> int:
-        return (eta + 1) * self.batch_size * self.group_size
+        return (eta + 1) * (self.batch_size + self.extra_groups) * self.members
 
 
 def draw_lengths(p: Preset, scen_index: int, n_groups: int, group0: int = 0):
-    """(prompt_len[n_groups], target_len[n_groups*G]) int32 for one scenario."""
+    """(prompt_len[n_groups], target_len[n_groups*(G + extra_members)]) int32 for one scenario."""
     sc = p.scenarios[scen_index]
-    G = p.group_size
+    G = p.members
     g = np.arange(group0, group0 + n_groups, dtype=np.int64)
     prompt = uniform_int(counter_u64(sc.seed, scen_index, g, np.zeros_like(g), STREAM_PROMPT),
                          p.prompt.lo, p.prompt.hi)
@@ -205,6 +213,11 @@ def preset(name: str, n_scenarios: Optional[int] = None) -> Preset:
         return Preset("C5", sc, 64, 8, LengthDist("uniform", 64, 512),
                       LengthDist("lognormal", median=768, cap=4096),
                       131_072, 15, 10)
+    if name == "C5R":
+        # C5 with App C's redundancy ratios (+1/16 of the batch, +1/16 of the group,
+        # rounded up to whole groups / members): 64 + 4 groups, 8 + 1 members
+        p = preset("C5", n_scenarios)
+        return dataclasses.replace(p, name="C5R", extra_groups=4, extra_members=1)
     raise ValueError(f"unknown preset {name}")
 
 
