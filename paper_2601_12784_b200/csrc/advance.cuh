@@ -182,7 +182,11 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
       for (int q = 0; q < kR; ++q) {
         const bool a = ((live[q] >> lane) & 1u) && D.loc[C.traj_off + rid[q]] == L_ABORTED;
         const unsigned am = __ballot_sync(0xffffffffu, a);
-        if (a) { release += k5 * (long long)(fin[q] - rem[q]); rem[q] = kDead; }   // p + gen
+        if (a) {
+          release += k5 * (long long)(fin[q] - rem[q]);                           // p + gen
+          D.gen[C.traj_off + rid[q]] = tq[q] - rem[q];                           // progress kept
+          rem[q] = kDead;
+        }
         live[q] &= ~am;
         nab += __popc(am);
       }
@@ -513,7 +517,11 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
         if (k < x.run_n) {
           rem = D.run_rem[lb + k]; id = D.run_id[lb + k];
           ab = D.loc[C.traj_off + id] == L_ABORTED;
-          if (ab) release += k5 * (long long)(D.prompt[C.grp_off + grp_of(P, id)] + D.T[C.traj_off + id] - rem);
+          if (ab) {
+            const int gj = D.T[C.traj_off + id] - rem;
+            release += k5 * (long long)(D.prompt[C.grp_off + grp_of(P, id)] + gj);
+            D.gen[C.traj_off + id] = gj;
+          }
         }
         const bool keep = k < x.run_n && !ab;
         const unsigned mk = __ballot_sync(0xffffffffu, keep);
