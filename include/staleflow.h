@@ -122,6 +122,19 @@ sf_status sf_publish_params(sf_ctx *ctx, int32_t scenario, int32_t new_version);
 sf_status sf_collect_batch(sf_ctx *ctx, int32_t scenario, int32_t cap, int32_t *v_buf, int32_t *group_ids,
                            int32_t *group_versions, int32_t *n_out);
 
+/* Filtering (P:413 (2)).  flags[a] != 0 marks group first_group + a of the scenario's pool as
+ * carrying no learning signal (e.g. identical rewards within the group, DAPO): when it completes
+ * its entry is aborted instead of Occupied -- a later Occupied entry moves forward into the hole
+ * (reading R-FILTER) -- and its members are dropped.  Host pointer, copied; may be
+ * called before or after the groups are submitted.  Errors: SF_E_RANGE. */
+sf_status sf_mark_filtered(sf_ctx *ctx, int32_t scenario, int32_t first_group, int32_t n_groups,
+                           const uint8_t *flags);
+/* Proactive filtering between windows of a tracked (Reserved or Occupied) group, e.g. one whose
+ * stragglers stall training (P:413 (2); SPEC abort S:96-103): its ledger entry is aborted as above
+ * and every member not yet consumed is Aborted (Abort commands for the in-flight ones).
+ * Errors: SF_E_INVALID if the group has no ledger entry (UnknownKey), SF_E_RANGE. */
+sf_status sf_filter_group(sf_ctx *ctx, int32_t scenario, int32_t group);
+
 /* Cumulative int64 metrics summed over scenarios into host out[len]; slot 29
  * counts poisoned scenarios and slot 30 is the maximum simulated time. */
 sf_status sf_read_metrics(sf_ctx *ctx, int64_t *out, int32_t len);

@@ -101,6 +101,9 @@ def load_oracle():
         "sfo_ledger_verify": (C.c_int, [P, I32]),
         "sfo_ledger_reserve": (C.c_int, [P, I32, I32, pI32, pI32]),
         "sfo_ledger_delete_relocate": (C.c_int, [P, I32]),
+        "sfo_ledger_abort": (C.c_int, [P, I32, pI32]),
+        "sfo_mark_filtered": (C.c_int, [P, I32, I32, I32, C.POINTER(C.c_uint8)]),
+        "sfo_filter_group": (C.c_int, [P, I32, I32]),
         "sfo_ledger_occupy": (C.c_int, [P, I32, I32, pI32, pI32]),
         "sfo_ledger_state": (C.c_int, [P, I32]),
         "sfo_ledger_consume": (C.c_int, [P, pI32, pI32]),
@@ -203,6 +206,13 @@ class OracleSim:
                                       _ptr(v, C.c_int32), _ptr(n, C.c_int32))
         return rc, int(vb[0]), g, v
 
+    def mark_filtered(self, scen: int, first_group: int, flags) -> int:
+        f = np.ascontiguousarray(flags, dtype=np.uint8)
+        return self.L.sfo_mark_filtered(self.h, scen, first_group, len(f), _ptr(f, C.c_uint8))
+
+    def filter_group(self, scen: int, group: int) -> int:
+        return self.L.sfo_filter_group(self.h, scen, group)
+
     def metrics(self, scen: Optional[int] = None) -> np.ndarray:
         out = np.zeros(METRICS_LEN, np.int64)
         if scen is None:
@@ -266,6 +276,12 @@ class Ledger:
 
     def delete_relocate(self, g: int) -> int:
         return self.L.sfo_ledger_delete_relocate(self.h, g)
+
+    def abort(self, g: int):
+        """abort a tracked entry; returns (rc, moves)."""
+        m = C.c_int32()
+        rc = self.L.sfo_ledger_abort(self.h, g, C.byref(m))
+        return rc, m.value
 
     def occupy(self, g: int, v: int):
         b, s = C.c_int32(), C.c_int32()

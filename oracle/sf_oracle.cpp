@@ -71,7 +71,7 @@ struct sfo_ledger {
   // repeatedly "scan buffers from smallest up to V_buf to find the earliest reserved entry B
   // satisfying V_B + eta >= V_buf, and move B to A's position" (A13: iterate to a fixpoint;
   // earliest buffer first, then lowest slot).  Returns the number of moves.
-  int delete_and_relocate(int b, int s) {
+  int delete_and_relocate(int b, int s, int *fhb = nullptr, int *fhs = nullptr) {
     buf[b][s] = Entry();
     int hb = b, hs = s, moves = 0;
     for (;;) {
@@ -90,7 +90,45 @@ struct sfo_ledger {
       }
       if (!found) break;
     }
+    if (fhb) { *fhb = hb; *fhs = hs; }
     return moves;
+  }
+  // Filtering (P:413 (2): "after abortion, occupied entries from later buffers can be moved
+  // forward to fill the empty slot"; SPEC abort op S:96-103), reading R-FILTER: the hole at
+  // (hb, hs) takes the Occupied entry of the earliest later buffer (lowest slot) whose version
+  // admits buffer hb (v <= hb; v + eta >= hb holds since it sat in a later buffer); repeated with
+  // the hole that move leaves.  Returns the number of moves.
+  int fill_forward(int hb, int hs) {
+    int moves = 0;
+    for (;;) {
+      bool found = false;
+      for (int bb = hb + 1; bb < (int)buf.size() && !found; ++bb) {
+        for (int ss = 0; ss < B; ++ss) {
+          const Entry &e = buf[bb][ss];
+          if (e.st == E_OCCUPIED && e.v <= hb) {
+            buf[hb][hs] = e;
+            buf[bb][ss] = Entry();
+            hb = bb; hs = ss; ++moves;
+            found = true;
+            break;
+          }
+        }
+      }
+      if (!found) break;
+    }
+    return moves;
+  }
+  // Abort a tracked entry: a Reserved one through delete_and_relocate, an Occupied
+  // one by emptying its slot; then fill_forward.  false if g has no entry (UnknownKey).
+  bool abort_entry(int g, int *moves) {
+    int b = -1, sl = -1;
+    if (!find(g, &b, &sl)) return false;
+    int hb = b, hs = sl, m = 0;
+    if (buf[b][sl].st == E_RESERVED) m = delete_and_relocate(b, sl, &hb, &hs);
+    else buf[b][sl] = Entry();
+    m += fill_forward(hb, hs);
+    if (moves) *moves = m;
+    return true;
   }
   // Occupy: "scans forward and greedily occupies the earliest available empty entry"
   // (from consumed_upto, lowest slot first).
@@ -315,7 +353,7 @@ struct Traj {
   int n_routes = 0, n_preempt = 0, n_interrupt = 0;
   int64_t t_complete = -1, ready = 0;
 };
-struct Group { int p = 0, v = -1, n_rewarded = 0, consumed_vbuf = -1; };
+struct Group { int p = 0, v = -1, n_rewarded = 0, consumed_vbuf = -1; bool filter = false, retired = false; };
 struct Arrival { int64_t t; int id; };
 struct Inst {
   int v = 0; int64_t kv = 0; std::vector<int> run; std::deque<int> wait; int c = 0;
@@ -361,10 +399,11 @@ int ctx_len(const Scen &s, int j) { return s.grp[s.traj[j].g].p + s.traj[j].gen;
 // Abort (P:473 footnote; Table 1 row P:577): trajectory j leaves for good.  On an instance it is
 // removed at that instance's next boundary; an arrival in transit is dropped at delivery; a
 // TS-resident one is dropped from the TS; a completed one's pending reward is ignored.
-void abort_member(Scen &s, int j) {
+void abort_member(Scen &s, int j, bool force = false) {
   Traj &tr = s.traj[j];
   const int st = tr.st;
-  if (st == L_ABORTED || st == L_CONSUMED || tr.rewarded) return;
+  // a rewarded member is kept unless its whole group is dropped (filtering, reading R-FILTER)
+  if (st == L_ABORTED || st == L_CONSUMED || (tr.rewarded && !force)) return;
   if (st == L_TRANSIT || st == L_WAIT || st == L_RUN) {
     log_cmd(s, CMD_ABORT, tr.inst, j);
     s.inst[tr.inst].acc -= 1;
@@ -377,6 +416,18 @@ void abort_member(Scen &s, int j) {
 
 void abort_group(Scen &s, int g) {
   for (int m = 0; m < s.G; ++m) abort_member(s, g * s.G + m);
+}
+
+// Filtering (P:413 (2), reading R-FILTER): group g's ledger entry is aborted (abort_entry) and
+// every member not yet consumed leaves (Abort commands for the in-flight ones); the group stops
+// counting toward the live-group cap.
+void filter_group(Scen &s, int g) {
+  int moves = 0;
+  if (!s.L.abort_entry(g, &moves)) { s.err = SFO_E_STATE; return; }
+  s.m[M_RELOCATIONS] += moves;
+  for (int m = 0; m < s.G; ++m) abort_member(s, g * s.G + m, true);
+  s.grp[g].retired = true;
+  s.live -= 1;
 }
 
 // Consume: retire the earliest Ready buffer as one batch -- its first Br Occupied entries in
@@ -632,6 +683,7 @@ void apply_reward(Scen &s, int j) {
   for (int m = 0; m < s.G; ++m) abort_member(s, g * s.G + m);
   int b = -1, sl = -1;
   if (!s.L.find(g, &b, &sl) || s.L.buf[b][sl].st != E_RESERVED) { s.err = SFO_E_STATE; return; }
+  if (gr.filter) { filter_group(s, g); return; }   // no learning signal (P:413 (2), DAPO): dropped
   s.m[M_RELOCATIONS] += s.L.delete_and_relocate(b, sl);
   int ob = -1, os = -1;
   if (!s.L.occupy(g, gr.v, &ob, &os)) { s.err = SFO_E_STATE; return; }
@@ -805,6 +857,25 @@ int sfo_collect_batch(sfo_sim *sim, int32_t k, int32_t cap, int32_t *v_buf, int3
   return s.err ? SFO_E_STATE : SFO_OK;
 }
 
+int sfo_mark_filtered(sfo_sim *sim, int32_t k, int32_t g0, int32_t n, const uint8_t *flags) {
+  if (!sim || k < 0 || k >= (int)sim->sc.size() || g0 < 0 || n < 0) return SFO_E_RANGE;
+  Scen &s = sim->sc[k];
+  if (s.err) return SFO_E_STATE;
+  if (g0 + n > s.pool_cap || (n > 0 && !flags)) return SFO_E_RANGE;
+  for (int a = 0; a < n; ++a) s.grp[g0 + a].filter = flags[a] != 0;
+  return SFO_OK;
+}
+
+int sfo_filter_group(sfo_sim *sim, int32_t k, int32_t g) {
+  if (!sim || k < 0 || k >= (int)sim->sc.size()) return SFO_E_RANGE;
+  Scen &s = sim->sc[k];
+  if (s.err) return SFO_E_STATE;
+  int b = -1, sl = -1;
+  if (g < 0 || g >= s.n_ingested || !s.L.find(g, &b, &sl)) return SFO_E_INVALID;   // UnknownKey
+  filter_group(s, g);
+  return s.err ? SFO_E_STATE : SFO_OK;
+}
+
 int sfo_read_scenario_metrics(sfo_sim *sim, int32_t k, int64_t *out, int32_t len) {
   if (!sim || k < 0 || k >= (int)sim->sc.size() || len < 0) return SFO_E_RANGE;
   const Scen &s = sim->sc[k];
@@ -901,6 +972,9 @@ int sfo_ledger_delete_relocate(sfo_ledger *L, int32_t g) {
   int b, s;
   if (!L->find(g, &b, &s) || L->buf[b][s].st != E_RESERVED) return SFO_E_INVALID;
   return L->delete_and_relocate(b, s);
+}
+int sfo_ledger_abort(sfo_ledger *L, int32_t g, int32_t *moves) {
+  return L->abort_entry(g, moves) ? SFO_OK : SFO_E_INVALID;
 }
 int sfo_ledger_occupy(sfo_ledger *L, int32_t g, int32_t v, int32_t *b, int32_t *s) {
   int ob, os;

@@ -54,6 +54,12 @@ int sfo_submit_prompts(sfo_sim *, int32_t scenario, int32_t n_groups, const int3
 /* Advance every scenario by n_windows snapshot periods; scenarios run on n_threads host threads. */
 int sfo_step(sfo_sim *, int32_t n_windows, int32_t n_threads);
 int sfo_publish_params(sfo_sim *, int32_t scenario, int32_t new_version);
+/* Filtering (P:413 (2)): flags[a] != 0 marks group first_group + a as carrying no learning signal
+ * (e.g. identical rewards, DAPO); such a group is dropped when it completes (reading R-FILTER). */
+int sfo_mark_filtered(sfo_sim *, int32_t scenario, int32_t first_group, int32_t n, const uint8_t *flags);
+/* Proactive filtering of a tracked (Reserved or Occupied) group between windows: its entry is
+ * aborted (ledger abort) and its members leave.  SFO_E_INVALID if the group has no entry. */
+int sfo_filter_group(sfo_sim *, int32_t scenario, int32_t group);
 int sfo_collect_batch(sfo_sim *, int32_t scenario, int32_t cap, int32_t *v_buf, int32_t *group_ids,
                       int32_t *group_versions, int32_t *n_out);
 /* metrics summed over scenarios (layout: DESIGN.md §6) */
@@ -64,7 +70,7 @@ int sfo_read_scenario_metrics(sfo_sim *, int32_t scenario, int64_t *out, int32_t
 int sfo_dump_lifecycles(sfo_sim *, int32_t scenario, int64_t *records, int64_t cap, int64_t *n);
 /* per consumed batch: v_buf, then B (group id, group version) pairs */
 int sfo_dump_batches(sfo_sim *, int32_t scenario, int32_t *out, int64_t cap, int64_t *n);
-/* 4 int64 per command: window, kind (1 Route, 2 Interrupt, 3 Pull), inst, traj (-1 for Pull) */
+/* 4 int64 per command: window, kind (1 Route, 2 Interrupt, 3 Pull, 4 Abort), inst, traj (-1 for Pull) */
 int sfo_dump_commands(sfo_sim *, int32_t scenario, int64_t *out, int64_t cap, int64_t *n);
 /* per-instance snapshot view: v, kv, n_run, n_wait, complete, state(0 idle,1 tick,2 pull), nb */
 int sfo_dump_instances(sfo_sim *, int32_t scenario, int64_t *out, int64_t cap, int64_t *n);
@@ -78,6 +84,9 @@ void sfo_ledger_free(sfo_ledger *);
 int sfo_ledger_verify(const sfo_ledger *, int32_t v);                           /* 1/0 */
 int sfo_ledger_reserve(sfo_ledger *, int32_t g, int32_t v, int32_t *b, int32_t *s);
 int sfo_ledger_delete_relocate(sfo_ledger *, int32_t g);
+/* abort a tracked entry: Reserved -> delete_and_relocate, Occupied -> emptied;
+ * then later Occupied entries move forward into the hole (reading R-FILTER); *moves = moves */
+int sfo_ledger_abort(sfo_ledger *, int32_t g, int32_t *moves);
 int sfo_ledger_occupy(sfo_ledger *, int32_t g, int32_t v, int32_t *b, int32_t *s);
 int sfo_ledger_state(const sfo_ledger *, int32_t b);  /* 0 Waiting, 1 Ready, 2 Stuck */
 /* first batch_size Occupied entries in slot order; returns the surplus (aborted) groups through

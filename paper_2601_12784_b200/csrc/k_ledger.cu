@@ -38,6 +38,31 @@ __global__ void k_collect(GParams P, Dev D, int s, int *out) {
   }
 }
 
+// Proactive filtering (P:413 (2)) of group g of scenario s between windows; out[0] = 0 done,
+// 1 the group has no ledger entry (not tracked: never routed, consumed or already dropped).
+__global__ void k_filter(GParams P, Dev D, int s, int g, int *out) {
+  const unsigned lane = lane_id();
+  const ScenConst C = D.sc[s];
+  ScenState &SS = D.ss[s];
+  bool tracked = g >= 0 && g < SS.n_ingested && D.cvbuf[C.grp_off + g] == -1 && D.led_b[C.grp_off + g] >= 0;
+  if (tracked) {
+    const long long at = ring_base(C, P.B, D.led_b[C.grp_off + g]) + D.led_s[C.grp_off + g];
+    tracked = D.led_st[at] != E_EMPTY && D.led_g[at] == g;
+  }
+  if (!tracked) { if (lane == 0) out[0] = 1; return; }
+  CmdLog cl{SS.cmd_hash, SS.cmd_n, SS.window, 0};
+  long long m_reloc = 0;
+  int err = 0;
+  filter_group(P, D, C, SS, g, SS.cu, cl, m_reloc, err);
+  if (lane == 0) {
+    out[0] = 0;
+    SS.cmd_hash = cl.hash; SS.cmd_n = cl.cmd_n;
+    SS.m[M_ABORTS] += cl.aborts;
+    SS.m[M_RELOCATIONS] += m_reloc;
+    if (err) SS.err = err;
+  }
+}
+
 // Sum of per-scenario metric vectors (integer, order independent) -> out[kMetrics].
 __global__ void k_reduce_metrics(Dev D, int n_scen, long long *out) {
   __shared__ unsigned long long acc[kMetrics];
@@ -112,6 +137,9 @@ void sf_launch_ledger(const sf::GParams &P, const sf::Dev &D, int n_scen, cudaSt
 }
 void sf_launch_collect(const sf::GParams &P, const sf::Dev &D, int scen, int *out_dev, cudaStream_t st) {
   sf::k_collect<<<1, 32, 0, st>>>(P, D, scen, out_dev);
+}
+void sf_launch_filter(const sf::GParams &P, const sf::Dev &D, int scen, int group, int *out_dev, cudaStream_t st) {
+  sf::k_filter<<<1, 32, 0, st>>>(P, D, scen, group, out_dev);
 }
 void sf_launch_reduce_metrics(const sf::Dev &D, int n_scen, long long *out_dev, cudaStream_t st) {
   sf::k_reduce_metrics<<<1, 1024, 0, st>>>(D, n_scen, out_dev);

@@ -30,12 +30,14 @@ __device__ __forceinline__ int first_slot(int B, Pred pred) {
   return -1;
 }
 
-static __device__ void complete_group(const GParams &P, const Dev &D, const ScenConst &C, ScenState &SS, int g, int cu,
-                               long long &m_reloc, long long &m_occ, int &err) {
+// Remove group g's Reserved entry at its ledger position and run the delete-and-relocate
+// cascade (reading A13); (hb, hs) returns the final hole.
+static __device__ void delete_relocate(const GParams &P, const Dev &D, const ScenConst &C, int g, int cu, int &hb,
+                                       int &hs, long long &m_reloc, int &err) {
   const unsigned lane = lane_id();
   const int B = P.B, eta = C.eta;
-  int hb = D.led_b[C.grp_off + g], hs = D.led_s[C.grp_off + g];
-  const int vg = D.gv[C.grp_off + g];
+  hb = D.led_b[C.grp_off + g];
+  hs = D.led_s[C.grp_off + g];
   {
     const long long base = ring_base(C, B, hb);
     if (D.led_st[base + hs] != E_RESERVED || D.led_g[base + hs] != g) { err = ERR_LEDGER; return; }
@@ -46,7 +48,6 @@ static __device__ void complete_group(const GParams &P, const Dev &D, const Scen
     }
     __syncwarp();
   }
-  // delete-and-relocate cascade (reading A13)
   for (;;) {
     int fb = -1, fs = -1;
     for (int bb = cu; bb < hb; ++bb) {
@@ -75,6 +76,16 @@ static __device__ void complete_group(const GParams &P, const Dev &D, const Scen
     hs = fs;
     ++m_reloc;
   }
+}
+
+static __device__ void complete_group(const GParams &P, const Dev &D, const ScenConst &C, ScenState &SS, int g, int cu,
+                               long long &m_reloc, long long &m_occ, int &err) {
+  const unsigned lane = lane_id();
+  const int B = P.B, eta = C.eta;
+  const int vg = D.gv[C.grp_off + g];
+  int hb, hs;
+  delete_relocate(P, D, C, g, cu, hb, hs, m_reloc, err);
+  if (err) return;
   // Occupy: earliest buffer >= cu with an empty slot, lowest slot
   int ob = -1, os = -1;
   for (int b = cu; b <= cu + eta; ++b) {
@@ -96,6 +107,69 @@ static __device__ void complete_group(const GParams &P, const Dev &D, const Scen
   }
   __syncwarp();
   ++m_occ;
+}
+
+// Filtering (P:413 (2), reading R-FILTER): the hole at (hb, hs) takes the Occupied entry of the
+// earliest later buffer (lowest slot) with version <= hb, repeated with the hole each move leaves.
+static __device__ void fill_forward(const GParams &P, const Dev &D, const ScenConst &C, int cu, int hb, int hs,
+                                    long long &m_reloc) {
+  const unsigned lane = lane_id();
+  const int B = P.B, eta = C.eta;
+  for (;;) {
+    int fb = -1, fs = -1;
+    for (int bb = hb + 1; bb <= cu + eta; ++bb) {
+      if (D.led_nocc[C.ring_off + bb % (eta + 1)] == 0) continue;
+      const long long base = ring_base(C, B, bb);
+      const int hole = hb;
+      const int sl = first_slot(B, [&](int x) { return D.led_st[base + x] == E_OCCUPIED && D.led_v[base + x] <= hole; });
+      if (sl >= 0) { fb = bb; fs = sl; break; }
+    }
+    if (fb < 0) break;
+    const long long src = ring_base(C, B, fb) + fs, dst = ring_base(C, B, hb) + hs;
+    const int mg = D.led_g[src], mv = D.led_v[src];
+    __syncwarp();
+    if (lane == 0) {
+      D.led_st[dst] = E_OCCUPIED; D.led_g[dst] = mg; D.led_v[dst] = mv;
+      D.led_st[src] = E_EMPTY; D.led_g[src] = -1; D.led_v[src] = -1;
+      D.led_nocc[C.ring_off + hb % (eta + 1)] += 1;
+      D.led_nocc[C.ring_off + fb % (eta + 1)] -= 1;
+      D.led_b[C.grp_off + mg] = hb;
+      D.led_s[C.grp_off + mg] = hs;
+    }
+    __syncwarp();
+    hb = fb;
+    hs = fs;
+    ++m_reloc;
+  }
+}
+
+// Drop a tracked group (filtering, P:413 (2), reading R-FILTER): abort its ledger entry (Reserved:
+// delete-and-relocate; Occupied: emptied), move later Occupied entries forward into the hole, and
+// Abort every member not yet consumed; the group leaves the live-group count.
+static __device__ void filter_group(const GParams &P, const Dev &D, const ScenConst &C, ScenState &SS, int g, int cu,
+                                    CmdLog &cl, long long &m_reloc, int &err) {
+  const unsigned lane = lane_id();
+  int hb = D.led_b[C.grp_off + g], hs = D.led_s[C.grp_off + g];
+  const long long at = ring_base(C, P.B, hb) + hs;
+  if (D.led_st[at] == E_RESERVED) {
+    delete_relocate(P, D, C, g, cu, hb, hs, m_reloc, err);
+    if (err) return;
+  } else {
+    if (D.led_st[at] != E_OCCUPIED || D.led_g[at] != g) { err = ERR_LEDGER; return; }
+    __syncwarp();
+    if (lane == 0) {
+      D.led_st[at] = E_EMPTY; D.led_g[at] = -1; D.led_v[at] = -1;
+      D.led_nocc[C.ring_off + hb % (C.eta + 1)] -= 1;
+    }
+    __syncwarp();
+  }
+  fill_forward(P, D, C, cu, hb, hs, m_reloc);
+  for (int m = 0; m < P.G; ++m) abort_member(P, D, C, cl, g * P.G + m, true);
+  if (lane == 0) {
+    D.cvbuf[C.grp_off + g] = -2;                  // retired without consumption
+    SS.live -= 1;
+  }
+  __syncwarp();
 }
 
 constexpr int kEvStage = 256;     // reward events staged per warp in shared memory
@@ -151,7 +225,7 @@ __device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, 
       // redundancy: the reward of an aborted member is ignored, and inside this batch the
       // members of a group past its Gr-th reward are aborted when the group completes
       bool eff = ok;
-      if (P.red && ok) eff = D.loc[C.traj_off + id] != L_ABORTED;
+      if (P.abortable && ok) eff = D.loc[C.traj_off + id] != L_ABORTED;
       const int nrw = eff ? D.n_rew[C.grp_off + g] : 0;
       const unsigned same = __match_any_sync(0xffffffffu, eff ? g : -1 - (int)lane);
       const int nr = nrw + 1 + __popc(same & lanemask_lt());
@@ -165,7 +239,8 @@ __device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, 
         const int gc = __shfl_sync(0xffffffffu, g, l);
         if (P.red)                                      // group-level redundancy: Abort the others
           for (int m = 0; m < P.G; ++m) abort_member(P, D, C, cl, gc * P.G + m);
-        complete_group(P, D, C, SS, gc, cu, m_reloc, m_occ, err);
+        if (P.filt && D.gfilt[C.grp_off + gc]) filter_group(P, D, C, SS, gc, cu, cl, m_reloc, err);
+        else complete_group(P, D, C, SS, gc, cu, m_reloc, m_occ, err);
         if (err) break;
       }
       np += __popc(okm);
@@ -191,7 +266,7 @@ __device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, 
       const int id = tmp[np];
       if (D.t_complete[C.traj_off + id] + P.R > t_end) break;
       const int g = grp_of(P, id);
-      if (P.red && D.loc[C.traj_off + id] == L_ABORTED) continue;     // ignored reward
+      if (P.abortable && D.loc[C.traj_off + id] == L_ABORTED) continue;     // ignored reward
       const int nr = D.n_rew[C.grp_off + g] + 1;
       __syncwarp();
       if (lane == 0) {
@@ -202,7 +277,8 @@ __device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, 
       if (nr == P.Gr) {
         if (P.red)
           for (int m = 0; m < P.G; ++m) abort_member(P, D, C, cl, g * P.G + m);
-        complete_group(P, D, C, SS, g, cu, m_reloc, m_occ, err);
+        if (P.filt && D.gfilt[C.grp_off + g]) filter_group(P, D, C, SS, g, cu, cl, m_reloc, err);
+        else complete_group(P, D, C, SS, g, cu, m_reloc, m_occ, err);
         if (err) break;
       }
     }

@@ -175,6 +175,8 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
   P.B = B; P.G = G;
   P.Br = cfg->batch_size; P.Gr = group_size;
   P.red = P.Br < B || P.Gr < G;
+  P.abortable = P.red;
+  P.filt = 0;
   P.k1 = cfg->k1_ps_per_tok; P.k2 = cfg->k2_ps; P.k3 = cfg->k3_ps; P.k4 = cfg->k4_ps;
   P.k5 = cfg->k5_tok; P.kp = cfg->kprefill_ps_per_tok; P.M = cfg->kv_budget_tok;
   P.k1i = (int)P.k1; P.k3i = (int)P.k3; P.kpi = (int)P.kp;
@@ -230,7 +232,8 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
        dalloc(c, &D.tinst, ntraj, 0xFF) && dalloc(c, &D.n_routes, ntraj, 0) && dalloc(c, &D.n_preempt, ntraj, 0) &&
        dalloc(c, &D.n_interrupt, ntraj, 0) && dalloc(c, &D.t_complete, ntraj, 0xFF) && dalloc(c, &D.ready, ntraj, 0);
   ok = ok && dalloc(c, &D.prompt, ngrp, 0) && dalloc(c, &D.gv, ngrp, 0xFF) && dalloc(c, &D.n_rew, ngrp, 0) &&
-       dalloc(c, &D.led_b, ngrp, 0xFF) && dalloc(c, &D.led_s, ngrp, 0xFF) && dalloc(c, &D.cvbuf, ngrp, 0xFF);
+       dalloc(c, &D.led_b, ngrp, 0xFF) && dalloc(c, &D.led_s, ngrp, 0xFF) && dalloc(c, &D.cvbuf, ngrp, 0xFF) &&
+       dalloc(c, &D.gfilt, ngrp, 0);
   ok = ok && dalloc(c, &D.iv, inst, 0) && dalloc(c, &D.ic, inst, 0) && dalloc(c, &D.ist, inst, 0) &&
        dalloc(c, &D.ipullv, inst, 0) && dalloc(c, &D.ipullpend, inst, 0) && dalloc(c, &D.iintkind, inst, 0) &&
        dalloc(c, &D.iintk, inst, 0) && dalloc(c, &D.irun_n, inst, 0) && dalloc(c, &D.iwhead, inst, 0) &&
@@ -402,6 +405,44 @@ sf_status sf_publish_params(sf_ctx *c, int32_t scenario, int32_t v) {
       !cuda_ok(c, cudaStreamSynchronize(c->stream), "sync"))
     return SF_E_CUDA;
   return SF_OK;
+}
+
+sf_status sf_mark_filtered(sf_ctx *c, int32_t scenario, int32_t first_group, int32_t n_groups, const uint8_t *flags) {
+  sf_status st = check_ctx(c);
+  if (st != SF_OK) return st;
+  DevGuard dg(c->device);
+  if (scenario < 0 || scenario >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
+  if (first_group < 0 || n_groups < 0 || (long long)first_group + n_groups > c->P.pool_cap)
+    return fail(c, SF_E_RANGE, "group range outside the pool");
+  if (n_groups == 0) return SF_OK;
+  if (!flags) return fail(c, SF_E_INVALID, "null argument");
+  bool any = false;
+  for (int a = 0; a < n_groups; ++a) any |= flags[a] != 0;
+  if (!cuda_ok(c, cudaMemcpyAsync(c->D.gfilt + (long long)c->hsc[scenario].grp_off + first_group, flags, n_groups,
+                                  cudaMemcpyHostToDevice, c->stream), "H2D filter flags") ||
+      !cuda_ok(c, cudaStreamSynchronize(c->stream), "sync"))
+    return SF_E_CUDA;
+  if (any) { c->P.filt = 1; c->P.abortable = 1; }
+  return SF_OK;
+}
+
+sf_status sf_filter_group(sf_ctx *c, int32_t scenario, int32_t group) {
+  sf_status st = check_ctx(c);
+  if (st != SF_OK) return st;
+  DevGuard dg(c->device);
+  if (scenario < 0 || scenario >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
+  c->P.abortable = 1;                                  // later rewards of its members are ignored
+  sf_launch_filter(c->P, c->D, scenario, group, c->d_collect, c->stream);
+  c->launches++;
+  int h = 0;
+  if (!cuda_ok(c, cudaGetLastError(), "filter launch") ||
+      !cuda_ok(c, cudaMemcpyAsync(&h, c->d_collect, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H") ||
+      !cuda_ok(c, cudaStreamSynchronize(c->stream), "sync"))
+    return SF_E_CUDA;
+  if (h != 0) return fail(c, SF_E_INVALID, "filter: group has no ledger entry (UnknownKey)");
+  long long m[sf::kMetrics];
+  if ((st = reduce_metrics_host(c, m)) != SF_OK) return st;
+  return check_errors(c, m);
 }
 
 sf_status sf_collect_batch(sf_ctx *c, int32_t scenario, int32_t cap, int32_t *v_buf, int32_t *group_ids,

@@ -27,7 +27,7 @@ EXPORTS = ["sf_create", "sf_destroy", "sf_submit_prompts", "sf_submit_prompts_ma
            "sf_publish_params", "sf_collect_batch", "sf_read_metrics", "sf_read_metrics_device",
            "sf_read_scenario_metrics", "sf_read_all_scenario_metrics", "sf_dump_lifecycles", "sf_dump_batches", "sf_dump_commands",
            "sf_dump_instances", "sf_kernel_launches", "sf_last_error", "sf_profile", "sf_profile_read",
-           "sf_fit_cost_model", "sf_plan_comm"]
+           "sf_fit_cost_model", "sf_plan_comm", "sf_mark_filtered", "sf_filter_group"]
 
 
 class SfConfig(C.Structure):
@@ -74,6 +74,8 @@ def load_library(path: str = LIB_PATH):
         "sf_step": (C.c_int, [P, I32, C.POINTER(SfStepStats)]),
         "sf_publish_params": (C.c_int, [P, I32, I32]),
         "sf_collect_batch": (C.c_int, [P, I32, I32, pI32, pI32, pI32, pI32]),
+        "sf_mark_filtered": (C.c_int, [P, I32, I32, I32, C.POINTER(C.c_uint8)]),
+        "sf_filter_group": (C.c_int, [P, I32, I32]),
         "sf_read_metrics": (C.c_int, [P, pI64, I32]),
         "sf_read_metrics_device": (C.c_int, [P, C.c_void_p]),
         "sf_read_scenario_metrics": (C.c_int, [P, I32, pI64, I32]),
@@ -225,6 +227,16 @@ class StaleFlow:
         rc = self.L.sf_collect_batch(self.h, scen, B, _p(vb, C.c_int32), _p(g, C.c_int32), _p(v, C.c_int32),
                                      _p(n, C.c_int32))
         return rc, int(vb[0]), g, v
+
+    def mark_filtered(self, scen: int, first_group: int, flags) -> None:
+        """Filtering (P:413 (2)): flags[a] != 0 drops group first_group + a when it completes."""
+        f = np.ascontiguousarray(flags, dtype=np.uint8)
+        self._check(self.L.sf_mark_filtered(self.h, scen, first_group, len(f), _p(f, C.c_uint8)), "sf_mark_filtered")
+
+    def filter_group(self, scen: int, group: int) -> int:
+        """Proactive filtering of a tracked group between windows; returns the sf_status
+        (SF_E_INVALID = -1 if the group has no ledger entry)."""
+        return self.L.sf_filter_group(self.h, scen, group)
 
     def metrics(self, scen: Optional[int] = None) -> np.ndarray:
         out = np.zeros(METRICS_LEN, np.int64)

@@ -39,7 +39,7 @@ MU, PHI_WAIT, PHI_TP = 0.3, 3, 5.0
 STRAT_R, STRAT_S, STRAT_M = 1, 2, 4  # bit = 1 -> StaleFlow strategy, 0 -> vanilla
 STRAT_SF = STRAT_R | STRAT_S | STRAT_M
 
-STREAM_PROMPT, STREAM_GROUP_Z, STREAM_MEMBER_Z, STREAM_TARGET = 1, 2, 3, 4
+STREAM_PROMPT, STREAM_GROUP_Z, STREAM_MEMBER_Z, STREAM_TARGET, STREAM_FILTER = 1, 2, 3, 4, 5
 
 
 def _splitmix64(x: np.ndarray) -> np.ndarray:
@@ -125,6 +125,7 @@ class Preset:
     phi_tp: float = PHI_TP
     extra_groups: int = 0                 # batch-level redundant rollout (App C)
     extra_members: int = 0                # group-level redundant rollout (P:473 footnote)
+    filter_prob: float = 0.0              # P(group carries no learning signal), filtered (P:413 (2))
 
     @property
     def members(self) -> int:
@@ -163,6 +164,15 @@ def draw_lengths(p: Preset, scen_index: int, n_groups: int, group0: int = 0):
         target = np.floor(x + 0.5)
         target = np.clip(target, 1, t.cap).astype(np.int64)
     return prompt.astype(np.int32), target.astype(np.int32)
+
+
+def draw_filter_flags(p: Preset, scen_index: int, n_groups: int, group0: int = 0) -> np.ndarray:
+    """uint8[n_groups]: 1 for a group whose rewards carry no learning signal (e.g. all identical,
+    DAPO dynamic sampling, P:413 (2)), drawn with probability p.filter_prob."""
+    sc = p.scenarios[scen_index]
+    g = np.arange(group0, group0 + n_groups, dtype=np.int64)
+    u = uniform_open01(counter_u64(sc.seed, scen_index, g, np.zeros_like(g), STREAM_FILTER))
+    return (u < p.filter_prob).astype(np.uint8)
 
 
 def sha256_arrays(*arrays) -> str:
@@ -215,9 +225,10 @@ def preset(name: str, n_scenarios: Optional[int] = None) -> Preset:
                       131_072, 15, 10)
     if name == "C5R":
         # C5 with App C's redundancy ratios (+1/16 of the batch, +1/16 of the group,
-        # rounded up to whole groups / members): 64 + 4 groups, 8 + 1 members
+        # rounded up to whole groups / members): 64 + 4 groups, 8 + 1 members; 1/16 of the groups
+        # filtered at completion (P:413 (2))
         p = preset("C5", n_scenarios)
-        return dataclasses.replace(p, name="C5R", extra_groups=4, extra_members=1)
+        return dataclasses.replace(p, name="C5R", extra_groups=4, extra_members=1, filter_prob=1 / 16)
     raise ValueError(f"unknown preset {name}")
 
 

@@ -32,6 +32,11 @@ def submit_both(o, g, p: W.Preset, scen_idx=None, n_groups=None):
         tgs.append(tg)
     rc = g.submit_many(np.arange(len(idx)), np.full(len(idx), ng), np.concatenate(prs), np.concatenate(tgs))
     assert rc == 0
+    if getattr(p, "filter_prob", 0.0) > 0:
+        for a, k in enumerate(idx):
+            f = W.draw_filter_flags(p, k, ng)
+            assert o.mark_filtered(a, 0, f) == 0
+            g.mark_filtered(a, 0, f)
 
 
 def first_cmd_divergence(co, cg):

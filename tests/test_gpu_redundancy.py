@@ -119,14 +119,58 @@ def test_c5r_full_size_sampled():
     n = len(p.scenarios)
     prs, tgs = zip(*[W.draw_lengths(p, k, p.pool_groups) for k in range(n)])
     assert g.submit_many(np.arange(n), np.full(n, p.pool_groups), np.concatenate(prs), np.concatenate(tgs)) == 0
+    flags = [W.draw_filter_flags(p, k, p.pool_groups) for k in range(n)]
+    for k in range(n):
+        g.mark_filtered(k, 0, flags[k])
     g.step(130)
     sample = sorted(random.Random(2027).sample(range(n), 32))
     o = OracleSim.from_preset(p, sample)
     for a, k in enumerate(sample):
         assert o.submit(a, prs[k], tgs[k]) == 0
+        assert o.mark_filtered(a, 0, flags[k]) == 0
     assert o.step(130, 8) == 0
     for a, k in enumerate(sample):
         mo, mg = o.metrics(a), g.metrics(k)
         assert (mo == mg).all(), f"scenario {k}: {np.nonzero(mo != mg)}"
         assert (o.lifecycles(a) == g.lifecycles(k)).all()
         assert (o.batches(a) == g.batches(k)).all()
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_completion_filter_fuzz(seed, launch_mode):
+    """Groups flagged as carrying no learning signal are dropped when they complete (P:413 (2)):
+    entry aborted, later Occupied entries moved forward, members aborted."""
+    rng = random.Random(9100 + seed)
+    B, G, eta = rng.randint(1, 4), rng.randint(1, 3), rng.randint(0, 2)
+    em, eb = rng.randint(0, 1), rng.randint(0, 1)
+    o, g = pair(rng.randint(1, 3), eta, G, B, eb, em, seed=seed, steps=8, strategy=rng.randint(0, 7),
+                M=rng.choice([300, 1 << 20]))
+    n_groups = (B + eb) * (8 + eta + 2)
+    fr = random.Random(seed + 17)
+    flags = np.array([fr.random() < 0.3 for _ in range(n_groups)], np.uint8)
+    assert o.mark_filtered(0, 0, flags) == 0
+    g.mark_filtered(0, 0, flags)
+    run_lockstep(o, g, [0], 200, every=2)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_proactive_filter_fuzz(seed, launch_mode):
+    """sf_filter_group between windows on random tracked (and untracked) groups, in lockstep."""
+    rng = random.Random(5500 + seed)
+    B, G, eta = rng.randint(1, 4), rng.randint(1, 3), rng.randint(0, 2)
+    o, g = pair(rng.randint(1, 3), eta, G, B, rng.randint(0, 1), rng.randint(0, 1), seed=seed, steps=8,
+                strategy=rng.randint(0, 7))
+    n_filtered = 0
+    for w in range(150):
+        assert o.step(1) == 0
+        g.step(1)
+        if rng.random() < 0.3:
+            lc = o.lifecycles(0)
+            tracked = sorted({int(x) for x in lc[lc[:, 5] >= 0][:, 1]})      # routed groups
+            cand = tracked if tracked and rng.random() < 0.8 else sorted({int(x) for x in lc[:, 1]})
+            grp = rng.choice(cand)
+            ro, rg = o.filter_group(0, grp), g.filter_group(0, grp)
+            assert ro == rg, (w, grp, ro, rg)
+            n_filtered += ro == 0
+        compare(o, g, [0], where=f"window {w}")
+    assert n_filtered > 0
