@@ -190,6 +190,17 @@ sf_status sf_plan_comm(int32_t n_slices, const double *slice_bytes, int32_t n_se
                        const uint8_t *holds, const double *bandwidth, const double *latency, int32_t n_req,
                        const int32_t *req_slice, const int32_t *req_receiver, int32_t *out_sender, double *acc);
 
+/* Parameter server: Push / Pull requests under a read-write lock with
+ * writer preference (a waiting Push blocks new Pulls), simulated over int64 ps.  Request k:
+ * kind[k] (0 Pull, 1 Push), issue time, duration, and for a Push the version it writes.  Outputs
+ * per request: t_start / t_end of its lock hold, version (a Pull: the version committed when its
+ * read starts; a Push: its own, committed at t_end), status (0, or -2 VersionSkip for a Push whose
+ * version is not the last accepted + 1; nothing else happens for it).  Host arrays, caller-owned.
+ * Errors: SF_E_INVALID (null pointer, bad kind, negative duration). */
+sf_status sf_ps_lock_sim(int32_t n, const int32_t *kind, const int64_t *t_issue, const int64_t *duration,
+                         const int32_t *push_version, int32_t v0, int64_t *t_start, int64_t *t_end,
+                         int32_t *version, int32_t *status);
+
 /* Message for the last failing call; owned by the context, valid until the next call. */
 const char *sf_last_error(const sf_ctx *ctx);
 

@@ -4,6 +4,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <deque>
+#include <functional>
+#include <numeric>
+#include <queue>
 #include <vector>
 
 #include "../../include/staleflow.h"
@@ -116,6 +120,72 @@ sf_status sf_plan_comm(int32_t n_slices, const double *slice_bytes, int32_t n_se
     acc[best] += slice_bytes[k] / bandwidth[e] + latency[e];
     out_sender[r] = best;
   }
+  return SF_OK;
+}
+
+// Parameter-server Push / Pull under a read-write lock with writer
+// preference, as a discrete-event simulation over int64 ps.  Requests are taken in
+// (t_issue, index) order; at equal times lock releases precede arrivals.  Grant rules: a Pull
+// iff no Push is active or waiting; a Push iff no Pull or Push is active and no earlier Push
+// waits; on a release a waiting Push goes first (once the readers drain), else all waiting
+// Pulls at once.  A Pull delivers the version committed at its start; a Push commits at its
+// end.  status[k] = -2 (VersionSkip) for a Push whose version is not the last accepted + 1.
+sf_status sf_ps_lock_sim(int32_t n, const int32_t *kind, const int64_t *t_issue, const int64_t *duration,
+                         const int32_t *push_version, int32_t v0, int64_t *t_start, int64_t *t_end,
+                         int32_t *version, int32_t *status) {
+  if (n < 0 || (n > 0 && (!kind || !t_issue || !duration || !push_version || !t_start || !t_end || !version ||
+                          !status)))
+    return SF_E_INVALID;
+  for (int k = 0; k < n; ++k)
+    if ((kind[k] != 0 && kind[k] != 1) || duration[k] < 0) return SF_E_INVALID;
+  std::vector<int> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return t_issue[a] < t_issue[b]; });
+  // release events (time, request) in time order; ties by request index
+  using Rel = std::pair<int64_t, int>;
+  std::priority_queue<Rel, std::vector<Rel>, std::greater<Rel>> rel;
+  std::deque<int> wait_w, wait_r;                  // waiting Pushes / Pulls, arrival order
+  int active_r = 0, active_w = -1;
+  int32_t accepted = v0, committed = v0;
+  for (int k = 0; k < n; ++k) { t_start[k] = -1; t_end[k] = -1; version[k] = -1; status[k] = 0; }
+  auto grant = [&](int k, int64_t now) {
+    t_start[k] = now;
+    t_end[k] = now + duration[k];
+    if (kind[k] == 1) { active_w = k; version[k] = push_version[k]; }
+    else { ++active_r; version[k] = committed; }
+    rel.push({t_end[k], k});
+  };
+  auto schedule = [&](int64_t now) {
+    if (active_w >= 0) return;
+    if (!wait_w.empty()) {
+      if (active_r == 0) { const int k = wait_w.front(); wait_w.pop_front(); grant(k, now); }
+      return;
+    }
+    while (!wait_r.empty()) { const int k = wait_r.front(); wait_r.pop_front(); grant(k, now); }
+  };
+  auto release_until = [&](int64_t t, bool all) {
+    while (!rel.empty() && (all || rel.top().first <= t)) {
+      const Rel r = rel.top();
+      rel.pop();
+      if (r.second == active_w) { committed = push_version[r.second]; active_w = -1; }
+      else --active_r;
+      schedule(r.first);
+    }
+  };
+  for (int k : order) {
+    const int64_t now = t_issue[k];
+    release_until(now, false);
+    if (kind[k] == 1) {
+      if (push_version[k] != accepted + 1) { status[k] = -2; continue; }   // VersionSkip
+      accepted = push_version[k];
+      if (active_w < 0 && active_r == 0 && wait_w.empty()) grant(k, now);
+      else wait_w.push_back(k);
+    } else {
+      if (active_w < 0 && wait_w.empty()) grant(k, now);
+      else wait_r.push_back(k);
+    }
+  }
+  release_until(0, true);
   return SF_OK;
 }
 

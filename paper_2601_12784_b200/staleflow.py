@@ -27,7 +27,8 @@ EXPORTS = ["sf_create", "sf_destroy", "sf_submit_prompts", "sf_submit_prompts_ma
            "sf_publish_params", "sf_collect_batch", "sf_read_metrics", "sf_read_metrics_device",
            "sf_read_scenario_metrics", "sf_read_all_scenario_metrics", "sf_dump_lifecycles", "sf_dump_batches", "sf_dump_commands",
            "sf_dump_instances", "sf_kernel_launches", "sf_last_error", "sf_profile", "sf_profile_read",
-           "sf_fit_cost_model", "sf_plan_comm", "sf_mark_filtered", "sf_filter_group"]
+           "sf_fit_cost_model", "sf_plan_comm", "sf_mark_filtered", "sf_filter_group",
+           "sf_ps_lock_sim"]
 
 
 class SfConfig(C.Structure):
@@ -89,6 +90,7 @@ def load_library(path: str = LIB_PATH):
         "sf_profile": (C.c_int, [P, I32]),
         "sf_fit_cost_model": (C.c_int, [I32, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double),
                                         C.POINTER(C.c_double)]),
+        "sf_ps_lock_sim": (C.c_int, [I32, pI32, pI64, pI64, pI32, I32, pI64, pI64, pI32, pI32]),
         "sf_plan_comm": (C.c_int, [I32, C.POINTER(C.c_double), I32, I32, C.POINTER(C.c_uint8),
                                    C.POINTER(C.c_double), C.POINTER(C.c_double), I32, pI32, pI32, pI32,
                                    C.POINTER(C.c_double)]),
@@ -323,3 +325,21 @@ def plan_comm(slice_bytes, holds, bandwidth, latency, req_slice, req_receiver):
     if rc != 0:
         raise SfError(f"sf_plan_comm: {STATUS.get(rc, rc)}")
     return out[: len(rs)], acc
+
+
+def ps_lock_sim(kind, t_issue, duration, push_version, v0: int = 0):
+    """Parameter-server Push/Pull under the writer-preferring read-write lock (include/staleflow.h
+    sf_ps_lock_sim).  Returns (t_start, t_end, version, status) int arrays."""
+    L = load_library()
+    k = np.ascontiguousarray(kind, dtype=np.int32)
+    n = len(k)
+    t = np.ascontiguousarray(t_issue, dtype=np.int64)
+    d = np.ascontiguousarray(duration, dtype=np.int64)
+    pv = np.ascontiguousarray(push_version, dtype=np.int32)
+    ts, te = np.zeros(n, np.int64), np.zeros(n, np.int64)
+    ver, st = np.zeros(n, np.int32), np.zeros(n, np.int32)
+    rc = L.sf_ps_lock_sim(n, _p(k, C.c_int32), _p(t, C.c_int64), _p(d, C.c_int64), _p(pv, C.c_int32), v0,
+                          _p(ts, C.c_int64), _p(te, C.c_int64), _p(ver, C.c_int32), _p(st, C.c_int32))
+    if rc != 0:
+        raise SfError(f"sf_ps_lock_sim: {STATUS.get(rc, rc)}")
+    return ts, te, ver, st

@@ -111,3 +111,77 @@ def test_plan_coverage_and_greedy_bound():                # acceptance 9
             rr_acc[s] += sizes[k]
         if all(sum(h) == n_sl for h in holds):            # identical senders: greedy is LPT-like
             assert max(acc) <= max(rr_acc) + 1e-9
+
+
+# ------------------------------------------------------------------ PS read-write lock
+def lock(kind, t, d, pv, v0=0):
+    a = [np.asarray(x).tolist() for x in SF.ps_lock_sim(kind, t, d, pv, v0)]
+    b = [list(x) for x in OT.ps_lock_sim(kind, t, d, pv, v0)]
+    assert a == b, (a, b)
+    return a
+
+
+def test_push_no_readers():
+    s, e, v, st = lock([1], [0], [10], [1])
+    assert (s, e, v, st) == ([0], [10], [1], [0])
+    s, e, v, st = lock([1, 0], [0, 10], [10, 1], [1, 0])  # a later Pull sees version 1
+    assert v[1] == 1
+
+
+def test_push_waits_for_active_pulls():                  # write begins after both complete
+    s, e, v, st = lock([0, 0, 1], [0, 1, 2], [5, 8, 3], [0, 0, 1])
+    assert s[2] == max(e[0], e[1]) == 9 and e[2] == 12
+
+
+def test_push_version_skip():
+    s, e, v, st = lock([1, 1], [0, 1], [1, 1], [1, 3])
+    assert st == [0, -2] and s[1] == -1
+
+
+def test_pulls_share_the_lock():                         # both complete after their own duration
+    s, e, v, st = lock([0, 0], [0, 0], [4, 7], [0, 0], v0=5)
+    assert s == [0, 0] and e == [4, 7] and v == [5, 5]
+
+
+def test_pull_during_push_gets_new_version():
+    s, e, v, st = lock([1, 0], [0, 2], [10, 3], [1, 0])
+    assert s[1] == 10 and v[1] == 1
+
+
+def test_writer_preference():                            # a waiting Push blocks new Pulls
+    s, e, v, st = lock([0, 1, 0], [0, 1, 2], [10, 5, 1], [0, 1, 0])
+    assert s[1] == 10 and s[2] == 15 and v[2] == 1
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_lock_fuzz_safety_and_parity(seed):
+    """Library == reference on random traces; lock safety (no Push interval overlaps another
+    interval), writer preference, version monotonicity."""
+    rng = random.Random(4000 + seed)
+    n = rng.randint(1, 60)
+    kind = [1 if rng.random() < 0.3 else 0 for _ in range(n)]
+    t = sorted(rng.randint(0, 200) for _ in range(n)) if seed % 2 else [rng.randint(0, 200) for _ in range(n)]
+    d = [rng.randint(0, 30) for _ in range(n)]
+    pv, nxt = [], 1
+    for k in kind:
+        if k == 1 and rng.random() < 0.9:
+            pv.append(nxt)
+            nxt += 1
+        else:
+            pv.append(rng.randint(0, 9) if k == 1 else 0)
+    s, e, v, st = lock(kind, t, d, pv)
+    ok = [k for k in range(n) if st[k] == 0]
+    for a in ok:
+        assert s[a] >= t[a]
+        for b in ok:
+            if a < b and (kind[a] == 1 or kind[b] == 1) and d[a] > 0 and d[b] > 0:
+                assert not (s[a] < e[b] and s[b] < e[a]), (a, b)
+    order = lambda k: (t[k], k)
+    for w in ok:
+        if kind[w] != 1:
+            continue
+        for r in ok:
+            if kind[r] == 0 and order(w) < order(r) and s[r] < s[w]:
+                assert s[r] < t[w] or (s[r] == t[w] and order(r) < order(w)), (w, r)   # granted before w arrived
+    pulls = sorted((s[k], v[k]) for k in ok if kind[k] == 0)
+    assert all(pulls[i][1] <= pulls[i + 1][1] for i in range(len(pulls) - 1))
