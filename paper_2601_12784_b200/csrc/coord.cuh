@@ -16,7 +16,7 @@ namespace sf {
 
 constexpr int kCoordWarps = 4; // scenarios per 128-thread block
 #ifndef SF_COORD_MINB
-#define SF_COORD_MINB 5      // blocks per SM for the 1-slot variant (register budget)
+#define SF_COORD_MINB 4      // blocks per SM for the 1-slot variant: 128 registers, no spills (measured)
 #endif
 constexpr int kArrStage = 128; // route records staged per warp in shared memory
 
@@ -39,7 +39,16 @@ struct Cyc {                   // lane-uniform per-cycle scalars
   int mlq_err;
   int use_bits;
   int red_w;                   // lanes holding instances (power of 2 >= min(I, 32)): reduction width
+#ifdef SF_TIMING_ROUTE
+  long long rt[6], rt_last;    // SF_TIMING_ROUTE builds: cycles per routing sub-step (tools/route_steps.py)
+#endif
 };
+
+#ifdef SF_TIMING_ROUTE
+#define SF_RT(k) do { if (tentative < 0) { const long long _n = clock64(); c.rt[k] += _n - c.rt_last; c.rt_last = _n; } } while (0)
+#else
+#define SF_RT(k) do { } while (0)
+#endif
 
 constexpr int kEmptyWords = 160;   // ledger empty-slot bitmap held in smem when (eta+1)*B <= 5120
 
@@ -192,24 +201,22 @@ static __device__ int route_group_batch(const GParams &P, const Dev &D, const Sc
   int jr = 0, done = 0;
   for (; done < nrem; ++done) {
     const double my = cnd ? sg.tab[jr][lane] : 0.0;
-    int sel = -1, last_ver = -1;
-    for (;;) {
-      int bv = 0x7fffffff, bi = 0x7fffffff;
-      double bd = 0.0;
-      if (cnd && S.v[0] > last_ver) { bv = S.v[0]; bd = my; bi = (int)lane; }
-      for (int o = 1; o < c.red_w; o <<= 1) {
-        const int ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const double od = __shfl_xor_sync(0xffffffffu, bd, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov < bv || (ov == bv && (od > bd || (od == bd && oi < bi)))) { bv = ov; bd = od; bi = oi; }
-      }
-      bv = __shfl_sync(0xffffffffu, bv, 0);
-      bd = __shfl_sync(0xffffffffu, bd, 0);
-      bi = __shfl_sync(0xffffffffu, bi, 0);
-      if (bv == 0x7fffffff) break;                     // withhold
-      if (bd >= thr) { sel = bi; break; }              // accept (A4)
-      last_ver = bv;
+    // waterfall as one reduction (see route_pass): lowest version with dT >= thr, then highest dT,
+    // then lowest id
+    int sel = -1;
+    int bk = (cnd && my >= thr) ? ((S.v[0] << 7) | (int)lane) : 0x7fffffff;
+    double bd = my;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      if (o >= c.red_w) break;
+      const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+      const bool better = ((ok >> 7) < (bk >> 7)) | (((ok >> 7) == (bk >> 7)) & ((od > bd) | ((od == bd) & (ok < bk))));
+      bk = better ? ok : bk;
+      bd = better ? od : bd;
     }
+    bk = __shfl_sync(0xffffffffu, bk, 0);
+    if (bk != 0x7fffffff) sel = bk & 127;
     if (sel < 0) { stopped = true; break; }
     if (tentative >= 0 && sel == tentative) { hit = true; return done + 1; }
     const int id = id0 + 1 + done;
@@ -256,19 +263,23 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
   int pass_group = -1, pass_vg = -1, routed = 0;
   unsigned vmask = verify_mask(sfree, c.eta);
   const int vbase = c.cu - c.eta;
-  int ideal_l = -1;                                  // Eq 4 depends on l only: reuse across group members
-  double thr_l = 0.0;
   double Tcur[KS];                                   // Eq 2 of each owned instance's current S
+  double Tn[KS];                                     // Eq 2 after routing the current item here (gamma)
 #pragma unroll
   for (int q = 0; q < KS; ++q) Tcur[q] = throughput_d(P, S.n[q], S.kv[q]);
   int k = 0;
   bool stop = false;
   int knext = 0;
+#ifdef SF_TIMING_ROUTE
+  c.rt_last = clock64();
+#endif
   while (knext < total && !stop) {
     const int k0 = knext;
-    // prefetch 32 MLQ items: lane a holds item k0 + a
+    // prefetch 32 MLQ items: lane a holds item k0 + a, with its Eq 4 threshold mu * ideal(l)
+    // (Alg 2 line P:1175) computed here, lane-parallel, off the decision chain
     int p_id = 0, p_vg = -1, p_l = 0;
     long long p_ready = 0;
+    double p_thr = 0.0;
     {
       const int kk = k0 + (int)lane;
       if (kk < total) {
@@ -277,10 +288,12 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
         p_vg = D.gv[C.grp_off + g];
         p_l = D.prompt[C.grp_off + g] + D.gen[C.traj_off + p_id];
         if (tentative < 0) p_ready = D.ready[C.traj_off + p_id];
+        if (!vanilla) p_thr = __dmul_rn(P.mu, ideal_gain_d(P, p_l));
       }
     }
     const int nb = min(32, total - k0);
     int a = 0;
+    SF_RT(0);
     for (; a < nb; ++a) {
       k = k0 + a;
       const int id = __shfl_sync(0xffffffffu, p_id, a);
@@ -299,7 +312,9 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
         any |= cand[q];
       }
       if (!__any_sync(0xffffffffu, any)) { stop = true; break; }
+      const double thr_a = __shfl_sync(0xffffffffu, p_thr, a);
       int sel = -1;
+      SF_RT(1);
       if (vanilla) {
         // fewest trajectories, lowest id
         long long best = 0x7fffffffffffffffLL;
@@ -313,40 +328,48 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
         best = __shfl_sync(0xffffffffu, best, 0);
         sel = (int)(best & 0xff);
       } else {
-        // Steps 2-4: waterfall over version groups.  One reduction on the
-        // key (lowest version, highest dT, lowest id) yields the best instance of the lowest
-        // remaining version group; accept it if it clears mu * ideal, else retry above that version.
-        if (l != ideal_l) { ideal_l = l; thr_l = __dmul_rn(P.mu, ideal_gain_d(P, l)); }
-        const double thr = thr_l;
-        double dT[KS];
+        // Steps 2-4: waterfall over version groups.  The first group (by
+        // ascending version) whose best dT clears thr = mu * ideal is the lowest version holding
+        // ANY candidate with dT >= thr, and that group's argmax (highest dT, lowest id) is such a
+        // candidate.  So one reduction on (version asc, dT desc, id asc) over the candidates with
+        // dT >= thr gives the waterfall's choice (no candidate: withhold).
+        const double thr = thr_a;
+        int bk = 0x7fffffff;                               // version << 7 | instance
+        double bd = 0.0;
 #pragma unroll
         for (int q = 0; q < KS; ++q) {
-          dT[q] = 0.0;
-          if (cand[q] && S.w[q] == 0 && S.kv[q] + (long long)P.k5 * l <= P.M)        // gamma (Eq 3)
-            dT[q] = __dsub_rn(throughput_d(P, S.n[q] + 1, S.kv[q] + (long long)P.k5 * l), Tcur[q]);
-        }
-        int last_ver = -1;
-        for (;;) {
-          int bv = 0x7fffffff, bi = 0x7fffffff;
-          double bd = 0.0;
-#pragma unroll
-          for (int q = 0; q < KS; ++q)
-            if (cand[q] && S.v[q] > last_ver &&
-                (S.v[q] < bv || (S.v[q] == bv && dT[q] > bd))) { bv = S.v[q]; bd = dT[q]; bi = (int)lane + 32 * q; }
-          for (int o = 1; o < c.red_w; o <<= 1) {
-            const int ov = __shfl_xor_sync(0xffffffffu, bv, o);
-            const double od = __shfl_xor_sync(0xffffffffu, bd, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (ov < bv || (ov == bv && (od > bd || (od == bd && oi < bi)))) { bv = ov; bd = od; bi = oi; }
+          Tn[q] = 0.0;
+          double d = 0.0;
+          if (cand[q] && S.w[q] == 0 && S.kv[q] + (long long)P.k5 * l <= P.M) {      // gamma (Eq 3)
+#ifdef SF_AB_NODIV
+            Tn[q] = (double)(S.n[q] + 1) * 1e-9 - (double)(S.kv[q] + (long long)P.k5 * l) * 1e-15;  // timing A/B only
+#else
+            Tn[q] = throughput_d(P, S.n[q] + 1, S.kv[q] + (long long)P.k5 * l);
+#endif
+            d = __dsub_rn(Tn[q], Tcur[q]);
           }
-          bv = __shfl_sync(0xffffffffu, bv, 0);
-          bd = __shfl_sync(0xffffffffu, bd, 0);
-          bi = __shfl_sync(0xffffffffu, bi, 0);
-          if (bv == 0x7fffffff) break;                     // no group accepted: withhold
-          if (bd >= thr) { sel = bi; break; }              // accept (reading A4)
-          last_ver = bv;
+          const int key = (S.v[q] << 7) | ((int)lane + 32 * q);
+          // branch-free (bitwise predicates + selects): data-dependent short-circuit branches
+          // would diverge the warp on the decision chain
+          const bool take = cand[q] & (d >= thr) & (((key >> 7) < (bk >> 7)) | (((key >> 7) == (bk >> 7)) & (d > bd)));
+          bk = take ? key : bk;
+          bd = take ? d : bd;
         }
+#ifndef SF_AB_NORED
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          if (o >= c.red_w) break;
+          const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+          const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+          const bool better = ((ok >> 7) < (bk >> 7)) | (((ok >> 7) == (bk >> 7)) & ((od > bd) | ((od == bd) & (ok < bk))));
+          bk = better ? ok : bk;
+          bd = better ? od : bd;
+        }
+#endif
+        bk = __shfl_sync(0xffffffffu, bk, 0);
+        if (bk != 0x7fffffff) sel = bk & 127;               // accept (reading A4)
       }
+      SF_RT(2);
       if (sel < 0) { stop = true; break; }
       // Step 5: route -- update S (Eq 3), Reserve if the group has no version yet.
       const int owner = sel & 31, qs = sel >> 5;
@@ -414,11 +437,15 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
 #pragma unroll
         for (int q = 0; q < KS; ++q)
           if (q == qs) {
-            if (gamma) { S.n[q] += 1; S.kv[q] += (long long)P.k5 * l; Tcur[q] = throughput_d(P, S.n[q], S.kv[q]); }
+            if (gamma) {
+              S.n[q] += 1; S.kv[q] += (long long)P.k5 * l;
+              Tcur[q] = vanilla ? throughput_d(P, S.n[q], S.kv[q]) : Tn[q];   // = T(n+1, kv+k5 l) (Eq 3's S')
+            }
             else S.w[q] += 1;
           }
       }
       if (tentative >= 0 && sel == tentative) return 1;
+      SF_RT(3);
       if (tentative < 0) {
       // issue Route(sel, id): t_arr = t_ready + r (A18)
       int aslot = 0;
@@ -450,6 +477,7 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
       log_cmd(P, D, C, c, CMD_ROUTE, sel, id);
       ++routed;
       }
+      SF_RT(4);
       // the rest of a versionless group (waterfall only), decided from precomputed gains
       if constexpr (KS == 1) {
         if (first_member && !vanilla && c.G > 1 && c.G <= kGMax && k >= c.n_v) {
@@ -457,13 +485,14 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
           if (nrem > 0) {
             bool hit = false, stopped = false;
             const int r = route_group_batch(P, D, C, c, S, Tcur[0], acc_delta[0], arrn[0], sg, id, vg, l, nrem,
-                                            thr_l, tentative, routed, hit, stopped);
+                                            thr_a, tentative, routed, hit, stopped);
             if (hit) return 1;
             a += r;
             if (stopped) { k = k0 + a + 1; stop = true; break; }
           }
         }
       }
+      SF_RT(5);
     }
     knext = k0 + a;
   }
@@ -603,6 +632,9 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
   c.vl_head = SS.vl_head; c.n_ingested = SS.n_ingested; c.window = SS.window; c.min_live_g = SS.min_live_g;
   c.hash = SS.cmd_hash; c.cmd_n = SS.cmd_n; c.reserves = 0; c.mlq_err = 0; c.n_v = 0; c.n_vl = 0;
   c.use_bits = 0;
+#ifdef SF_TIMING_ROUTE
+  for (int q = 0; q < 6; ++q) c.rt[q] = 0;
+#endif
   c.red_w = 1;
   while (c.red_w < min(C.I, 32)) c.red_w <<= 1;
   int live = SS.live, err = 0;
@@ -915,7 +947,11 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
     if (D.dbg) {
       D.dbg[8 * s + 0] = clock64() - t0_clk;
       D.dbg[8 * s + 1] = m_routes;
+#ifdef SF_TIMING_ROUTE
+      for (int q = 0; q < 6; ++q) D.dbg[8 * s + 2 + q] = c.rt[q];
+#else
       for (int q = 0; q < 6; ++q) D.dbg[8 * s + 2 + q] = ck[q];
+#endif
     }
 #endif
   }

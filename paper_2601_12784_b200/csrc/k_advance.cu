@@ -9,14 +9,20 @@ namespace sf {
 #endif
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, SF_ADV_MINB) k_advance(GParams P, Dev D, int n_inst_total) {
   __shared__ AdvStage stage_all[kWarpsPerBlock];
+  pdl_trigger();                                   // the ledger kernel may be scheduled now
   const int gi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (gi >= n_inst_total) return;
+  const int s = D.inst_scen[gi];
+  if (P.pdl) warp_wait_geq(&D.f_coord[s], P.epoch);     // this scenario's coordinator is done
   advance_instance(P, D, gi, stage_all[threadIdx.x >> 5]);
+  __threadfence();                                 // this lane's writes, device-wide
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) add_release(&D.f_adv[s], 1);
 }
 
 }  // namespace sf
 
 void sf_launch_advance(const sf::GParams &P, const sf::Dev &D, int n_inst_total, cudaStream_t st) {
   const int blocks = (n_inst_total + sf::kWarpsPerBlock - 1) / sf::kWarpsPerBlock;
-  sf::k_advance<<<blocks, 32 * sf::kWarpsPerBlock, 0, st>>>(P, D, n_inst_total);
+  sf_launch_pdl(sf::k_advance, blocks, 32 * sf::kWarpsPerBlock, st, P.pdl, P, D, n_inst_total);
 }

@@ -6,9 +6,14 @@ namespace sf {
 
 __global__ void __launch_bounds__(128) k_ledger(GParams P, Dev D) {
   __shared__ EvStage stage_all[kLedgerWarps];
+  pdl_trigger();                                   // the next window's coordinator may be scheduled
   const int s = blockIdx.x * kLedgerWarps + (threadIdx.x >> 5);
   if (s >= P.n_scen) return;
+  if (P.pdl) warp_wait_geq(&D.f_adv[s], P.epoch * D.sc[s].I);   // all its instances advanced
   ledger_scenario(P, D, s, stage_all[threadIdx.x >> 5]);
+  __threadfence();                                 // this lane's writes, device-wide
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) st_release(&D.f_led[s], P.epoch);
 }
 
 // External-trainer Consume for one scenario; out[0] = status (0 ok, 1 not ready),
@@ -133,7 +138,7 @@ __global__ void k_scatter_pool(Dev D, int G, const int *desc, int n_desc, const 
 }  // namespace sf
 
 void sf_launch_ledger(const sf::GParams &P, const sf::Dev &D, int n_scen, cudaStream_t st) {
-  sf::k_ledger<<<(n_scen + sf::kLedgerWarps - 1) / sf::kLedgerWarps, 128, 0, st>>>(P, D);
+  sf_launch_pdl(sf::k_ledger, (n_scen + sf::kLedgerWarps - 1) / sf::kLedgerWarps, 128, st, P.pdl, P, D);
 }
 void sf_launch_collect(const sf::GParams &P, const sf::Dev &D, int scen, int *out_dev, cudaStream_t st) {
   sf::k_collect<<<1, 32, 0, st>>>(P, D, scen, out_dev);

@@ -26,6 +26,8 @@ struct sf_ctx {
   int n_inst_total = 0;
   int max_inst = 1;
   int fused = 0;                      // launch mode: 1 = one fused window kernel (k_window)
+  int pdl = 1;                        // programmatic dependent launch between window kernels
+  long long epoch = 0;                // split-mode windows launched (PDL flag targets)
   int n_scen = 0;
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -216,6 +218,11 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
   // decode-step mode: closed-form skipping of quiet steps by default;
   // SF_ADVANCE=step processes every decode step individually (tests run both)
   c->P.skip = 1;
+  // programmatic dependent launch between the window kernels; SF_PDL=0 disables
+  c->pdl = 1;
+  if (const char *m = getenv("SF_PDL")) c->pdl = strcmp(m, "0") != 0;
+  c->P.pdl = 0;
+  c->P.epoch = 0;
   if (const char *m = getenv("SF_ADVANCE")) c->P.skip = strcmp(m, "step") != 0;
   if (const char *m = getenv("SF_LAUNCH")) {
     if (!strcmp(m, "split")) c->fused = 0;
@@ -240,7 +247,8 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
        dalloc(c, &D.iwn, inst, 0) && dalloc(c, &D.iarr_n, inst, 0) && dalloc(c, &D.ipv, inst, 0) &&
        dalloc(c, &D.iacc, inst, 0) && dalloc(c, &D.ikv, inst, 0) && dalloc(c, &D.inb, inst, 0) &&
        dalloc(c, &D.iuntil, inst, 0) && dalloc(c, &D.iprefill, inst, 0) && dalloc(c, &D.iabort, inst, 0) &&
-       dalloc(c, &D.iabort_arr, inst, 0);
+       dalloc(c, &D.iabort_arr, inst, 0) &&
+       dalloc(c, &D.f_coord, ns, 0) && dalloc(c, &D.f_adv, ns, 0) && dalloc(c, &D.f_led, ns, 0);
   ok = ok && dalloc(c, &D.run_id, list, 0) && dalloc(c, &D.run_rem, list, 0) && dalloc(c, &D.wait_id, list, 0) &&
        dalloc(c, &D.arr_id, list, 0) && dalloc(c, &D.arr_t, list, 0);
   ok = ok && dalloc(c, &D.led_st, led, 0) && dalloc(c, &D.led_g, led, 0xFF) && dalloc(c, &D.led_v, led, 0xFF) &&
@@ -356,15 +364,24 @@ sf_status sf_step(sf_ctx *c, int32_t n_windows, sf_step_stats *out) {
     prof_mark(c, 3);
     c->launches += 1;
   }
+  // Split mode: three kernels per window.  With PDL each kernel may start while its predecessor
+  // runs and waits per scenario on the progress flags (epoch = split windows so far), so a
+  // scenario's advance starts when ITS coordinator is done instead of after the slowest one.
+  // Profiling (events between kernels) serializes the launches.
+  const int pdl = c->pdl && !c->prof_on;
   for (int w = 0; w < (c->fused ? 0 : n_windows); ++w) {
+    GParams P = c->P;
+    P.epoch = ++c->epoch;
+    P.pdl = pdl && w > 0;                 // the first coordinator follows arbitrary stream work
     prof_mark(c, 0);
-    sf_launch_begin_coord(c->P, c->D, c->n_scen, c->max_inst, c->stream);
+    sf_launch_begin_coord(P, c->D, c->n_scen, c->max_inst, c->stream);
     prof_mark(c, 0);
+    P.pdl = pdl;
     prof_mark(c, 1);
-    sf_launch_advance(c->P, c->D, c->n_inst_total, c->stream);
+    sf_launch_advance(P, c->D, c->n_inst_total, c->stream);
     prof_mark(c, 1);
     prof_mark(c, 2);
-    sf_launch_ledger(c->P, c->D, c->n_scen, c->stream);
+    sf_launch_ledger(P, c->D, c->n_scen, c->stream);
     prof_mark(c, 2);
     c->launches += 3;
   }
