@@ -381,18 +381,28 @@ struct Scen {
   std::vector<Ev> rewards;
   std::vector<int> batches;
   std::vector<int64_t> cmds;
-  uint64_t cmd_hash = 1469598103934665603ULL;
+  uint64_t cmd_hash = 0;
   int64_t m[SFO_METRICS_LEN];
   int err = 0;
 };
 
+// Command checksum: the sum mod 2^64 of one mixed word per record, keyed by the
+// record's index in the scenario's command stream (so reordering changes it).
+uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+uint64_t record_hash(uint64_t index, int64_t window, int kind, int inst, int traj) {
+  const uint64_t a = (uint64_t)window * 0x9E3779B97F4A7C15ULL + index;
+  const uint64_t b = ((uint64_t)(uint32_t)traj << 32) | ((uint64_t)(uint32_t)kind << 24) | ((uint64_t)(uint32_t)inst & 0xffffffULL);
+  return mix64(mix64(a) ^ b);
+}
 void log_cmd(Scen &s, int kind, int inst, int traj) {
+  const uint64_t index = s.cmds.size() / 4;
+  s.cmd_hash += record_hash(index, s.window, kind, inst, traj);
   int64_t w[4] = {s.window, kind, inst, traj};
-  for (int k = 0; k < 4; ++k) {
-    s.cmds.push_back(w[k]);
-    s.cmd_hash ^= (uint64_t)w[k];
-    s.cmd_hash *= 1099511628211ULL;          // FNV-1a 64 over the 4 words of each record
-  }
+  for (int k = 0; k < 4; ++k) s.cmds.push_back(w[k]);
 }
 int ctx_len(const Scen &s, int j) { return s.grp[s.traj[j].g].p + s.traj[j].gen; }
 

@@ -87,8 +87,8 @@ __device__ __forceinline__ unsigned verify_mask(const int *sfree, int eta) {
 
 __device__ __forceinline__ void log_cmd(const GParams &P, const Dev &D, const ScenConst &C, Cyc &c, int kind,
                                         int inst, int traj) {
-  c.hash = fnv_words(c.hash, c.window, kind, inst, traj);
-  if (lane_id() == 0 && c.cmd_n < P.cmdlog_cap) {
+  c.hash += record_hash(c.cmd_n, c.window, kind, inst, traj);
+  if (c.cmd_n < P.cmdlog_cap && lane_id() == 0) {
     long long *r = D.cmdlog + C.cmd_off + 4LL * c.cmd_n;
     r[0] = c.window; r[1] = kind; r[2] = inst; r[3] = traj;
   }
@@ -251,6 +251,127 @@ static __device__ int route_group_batch(const GParams &P, const Dev &D, const Sc
   return done;
 }
 
+// Versioned MLQ items with few instances (I <= kRep, one instance per lane, Alg 2 waterfall):
+// lane a holds prefetched item k0 + a plus, for every instance q, its version and its item's Eq 3
+// gain and Eq 2 value there if routed (dT[q], Tn[q]).  A decision is the waterfall evaluated
+// lane-locally in the item's lane and broadcast; the chosen instance's snapshot entry is read from
+// its owner lane (shuffles), the owner applies the route, and every lane recomputes only its own
+// item's gain on the chosen instance (operation trees as in the one-at-a-time pass, so the
+// decisions are the same bit for bit).  Items are consumed in MLQ order until one is not routed
+// (*stop) or, in an Alg 3 trial, one is routed to the tentative instance (*hit).  Returns the
+// items decided (routed, plus the failing one if *stop).  Command records are hashed lane-parallel
+// after the loop.
+constexpr int kRep = 4;
+static __device__ int route_versioned_rep(const GParams &P, const Dev &D, const ScenConst &C, Cyc &c, InstRegs<1> &S,
+                                          double &Tcur, int &acc_delta, int &arrn, Stage &sg, int tentative, int nbv,
+                                          int p_id, int p_vg, int p_l, long long p_ready, double p_thr, int &routed,
+                                          bool &stop, bool &hit) {
+  const unsigned lane = lane_id();
+  const int I = c.I;
+  int rv[kRep];
+  double dT[kRep], Tn[kRep];
+  unsigned cmask = 0;                                   // check_routable for a versioned item: v_i >= v_g
+  const long long k5l = (long long)P.k5 * p_l;
+#pragma unroll
+  for (int q = 0; q < kRep; ++q) {
+    rv[q] = __shfl_sync(0xffffffffu, S.v[0], q);
+    const int nq = __shfl_sync(0xffffffffu, S.n[0], q);
+    const int wq = __shfl_sync(0xffffffffu, S.w[0], q);
+    const long long kvq = __shfl_sync(0xffffffffu, S.kv[0], q);
+    const double Tq = __shfl_sync(0xffffffffu, Tcur, q);
+    const bool cq = q < I && rv[q] >= p_vg;
+    cmask |= (unsigned)cq << q;
+    dT[q] = 0.0;
+    Tn[q] = 0.0;
+    if (cq && wq == 0 && kvq + k5l <= P.M) {                                           // gamma (Eq 3)
+      Tn[q] = throughput_d(P, nq + 1, kvq + k5l);
+      dT[q] = __dsub_rn(Tn[q], Tq);
+    }
+  }
+  int *const arr_id0 = D.arr_id + C.list_off;
+  long long *const arr_t0 = D.arr_t + C.list_off;
+  int a = 0, my_sel = 0;                                // my_sel: the instance this lane's item went to
+  SF_RT(0);
+  for (; a < nbv; ++a) {
+    // waterfall in this lane (meaningful in lane a): lowest version with dT >= thr, highest dT, lowest id
+    int bk = 0x7fffffff;
+    double bd = 0.0, bt = 0.0;
+#pragma unroll
+    for (int q = 0; q < kRep; ++q) {
+      const int key = (rv[q] << 7) | q;
+      const bool take = ((cmask >> q) & 1u) & (dT[q] >= p_thr) &
+                        (((key >> 7) < (bk >> 7)) | (((key >> 7) == (bk >> 7)) & (dT[q] > bd)));
+      bk = take ? key : bk;
+      bd = take ? dT[q] : bd;
+      bt = take ? Tn[q] : bt;
+    }
+    const int sel = __shfl_sync(0xffffffffu, bk == 0x7fffffff ? -1 : (bk & 127), a);
+    if (sel < 0) { stop = true; break; }                 // no candidate / none clears thr
+    if (tentative >= 0 && sel == tentative) { hit = true; return a + 1; }
+    SF_RT(1);
+    // the chosen instance's snapshot entry, from its owner lane; lane a's T(n+1, kv+k5 l) there
+    const int la = __shfl_sync(0xffffffffu, p_l, a);
+    const double tb = __shfl_sync(0xffffffffu, bt, a);
+    int ns = __shfl_sync(0xffffffffu, S.n[0], sel);
+    int ws = __shfl_sync(0xffffffffu, S.w[0], sel);
+    long long kvs = __shfl_sync(0xffffffffu, S.kv[0], sel);
+    double Ts = __shfl_sync(0xffffffffu, Tcur, sel);
+    const int aslot = __shfl_sync(0xffffffffu, arrn, sel);
+    const long long k5la = (long long)P.k5 * la;
+    const bool gamma = ws == 0 && kvs + k5la <= P.M;     // Step 5: Eq 3's S'
+    if (gamma) { ns += 1; kvs += k5la; Ts = tb; } else { ws += 1; }
+    if ((int)lane == sel) { S.n[0] = ns; S.w[0] = ws; S.kv[0] = kvs; Tcur = Ts; arrn += 1; acc_delta += 1; }
+    SF_RT(2);
+    double ds = 0.0, tn = 0.0;
+    if (((cmask >> sel) & 1u) && ws == 0 && kvs + k5l <= P.M) {
+      tn = throughput_d(P, ns + 1, kvs + k5l);
+      ds = __dsub_rn(tn, Ts);
+    }
+#pragma unroll
+    for (int q = 0; q < kRep; ++q)
+      if (q == sel) { dT[q] = ds; Tn[q] = tn; }
+    SF_RT(3);
+    if (tentative < 0) {
+      // issue Route(sel, id) from the item's lane: t_arr = t_ready + r (A18); its command record
+      // is hashed / logged after the loop, lane-parallel
+      if ((int)lane == a) {
+        my_sel = sel;
+        const long long j = C.traj_off + p_id;
+        const long long t_arr = max(c.t, p_ready) + P.r;
+        D.loc[j] = L_TRANSIT;
+        D.tinst[j] = (short)sel;
+        atomicAdd(&D.n_routes[j], 1);
+        const int ao = sel * C.cap + aslot;               // < I (eta+1) B G < 2^31 (sf_create)
+        arr_id0[ao] = p_id;
+        arr_t0[ao] = t_arr;
+        if (routed < kArrStage) {
+          sg.arr_t[routed] = t_arr;
+          sg.arr_id[routed] = p_id;
+          sg.arr_inst[routed] = (short)sel;
+        }
+        atomicAnd(&D.tsv_bits[C.bits_off + (p_id >> 5)], ~(1u << (p_id & 31)));
+      }
+      SF_RT(4);
+      ++routed;
+    }
+    SF_RT(5);
+  }
+  if (tentative < 0 && a > 0) {
+    // Route records of items 0 .. a-1 (lane = position in the command stream after cmd_n)
+    const bool mine = (int)lane < a;
+    const long long idx = c.cmd_n + lane;
+    const unsigned long long h = mine ? record_hash(idx, c.window, CMD_ROUTE, my_sel, p_id) : 0ULL;
+    if (mine && idx < P.cmdlog_cap) {
+      long long *r = D.cmdlog + C.cmd_off + 4LL * idx;
+      r[0] = c.window; r[1] = CMD_ROUTE; r[2] = my_sel; r[3] = p_id;
+    }
+    c.hash += warp_sum(h);
+    c.cmd_n += a;
+  }
+  __syncwarp();
+  return stop ? a + 1 : a;
+}
+
 // One routing pass (Alg 2, or vanilla §6.5) over the MLQ = [versioned n_v items] ++
 // [versionless groups vl_head..n_ingested).  tentative >= 0: Alg 3 trial for that instance on
 // scratch state, returns 1 as soon as a route targets it (early exit allowed).
@@ -294,6 +415,22 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
     const int nb = min(32, total - k0);
     int a = 0;
     SF_RT(0);
+    if constexpr (KS == 1) {
+#ifndef SF_NO_REP
+      if (!vanilla && c.I <= kRep && k0 < c.n_v) {
+#else
+      if (false) {
+#endif
+        const int nbv = min(nb, c.n_v - k0);
+        bool hit = false;
+        const int done = route_versioned_rep(P, D, C, c, S, Tcur[0], acc_delta[0], arrn[0], sg, tentative, nbv, p_id,
+                                             p_vg, p_l, p_ready, p_thr, routed, stop, hit);
+        if (hit) return 1;
+        if (stop) { k = k0 + done - 1; break; }
+        knext = k0 + done;
+        continue;
+      }
+    }
     for (; a < nb; ++a) {
       k = k0 + a;
       const int id = __shfl_sync(0xffffffffu, p_id, a);

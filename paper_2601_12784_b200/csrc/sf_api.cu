@@ -204,6 +204,10 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
       return SF_E_INVALID;
     }
     S.cap = (S.eta + 1) * B * G;
+    if ((long long)S.I * S.cap >= (1LL << 31)) {          // 32-bit per-scenario list offsets
+      delete c;
+      return SF_E_INVALID;
+    }
     S.inst_off = (int)inst; S.grp_off = s * P.pool_cap; S.led_off = (int)led; S.ring_off = (int)ring;
     S.traj_off = (long long)s * pool_traj; S.list_off = list; S.bits_off = bits; S.mlq_off = mlq;
     S.ev_off = ev; S.batch_off = batch; S.cmd_off = cmd;
@@ -274,7 +278,6 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
     for (int i = 0; i < c->hsc[s].I; ++i) hinst_scen[c->hsc[s].inst_off + i] = s;
   std::vector<ScenState> hss(ns);
   std::memset(hss.data(), 0, sizeof(ScenState) * ns);
-  for (int s = 0; s < ns; ++s) hss[s].cmd_hash = 1469598103934665603ULL;   // FNV-1a offset (§3.4)
   bool cp = cudaMemcpyAsync(dsc, c->hsc.data(), sizeof(ScenConst) * ns, cudaMemcpyHostToDevice, c->stream) == cudaSuccess &&
             cudaMemcpyAsync(dss, hss.data(), sizeof(ScenState) * ns, cudaMemcpyHostToDevice, c->stream) == cudaSuccess &&
             cudaMemcpyAsync(dinst_scen, hinst_scen.data(), sizeof(int) * inst, cudaMemcpyHostToDevice, c->stream) == cudaSuccess &&

@@ -22,7 +22,7 @@ for w in range(100):
     if w >= 5:
         rows.append(out.copy())
 a = np.concatenate(rows)
-print("cols: total routes prefetch item+cand dT+reduce update writes+hash group_batch")
+print("cols: total routes [rep path: gather+init, waterfall+bcast, update, divisions, records, hash] (route_steps)")
 for t in np.argsort(-a[:, 0])[:10]:
     r = a[t]
     print(r.tolist(), "per route:", (r[2:] / max(r[1], 1)).round(0).tolist())
