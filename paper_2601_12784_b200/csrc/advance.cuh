@@ -24,20 +24,20 @@ constexpr int kWarpsPerBlock = 8;
 struct InstState {
   int st, pullv, pullpend, intkind, intk, cc, v, run_n, whead, wn, arr_n, arr_head;
   int abortn, abortarr;                     // pending Aborts: run/wait members, undelivered arrivals
+  int evn;                                  // completion events in this instance's segment (D.iev)
   long long nb, until, kv, prefill, t_cmd;
   long long ticks, iters, tokens, comps, preempts;
 };
 
-__device__ __forceinline__ void emit_completion(const GParams &P, const Dev &D, const ScenConst &C, ScenState &SS,
-                                                int id, long long b, long long &release) {
+// completion of run entry (id, T, fin = p + T) at boundary b; event slot e of the instance segment
+__device__ __forceinline__ void emit_completion(const Dev &D, const ScenConst &C, long long lb, int id, int Tj, int fin,
+                                                long long b, int e, long long k5, long long &release) {
   const long long j = C.traj_off + id;
-  const int Tj = D.T[j];
-  release += (long long)P.k5 * (long long)(D.prompt[C.grp_off + grp_of(P, id)] + Tj);
+  release += k5 * (long long)fin;
   D.gen[j] = Tj;
   D.loc[j] = L_DONE;
   D.t_complete[j] = b;                      // reward due at b + R
-  const int e = atomicAdd(&SS.ev_n, 1);
-  D.ev_id[C.ev_off + e] = id;
+  D.iev[lb + e] = id;
 }
 
 // B1 (Abort, reading R-ABORT): drop the aborted members from the wait ring, FIFO order kept
@@ -85,13 +85,12 @@ struct AdvStage {
   int ev[kEvBuf];
 };
 
-__device__ __forceinline__ void flush_events(const Dev &D, const ScenConst &C, ScenState &SS, const int *ev, int &n) {
+// append n buffered completion events to this instance's segment (single writer: no atomics)
+__device__ __forceinline__ void flush_events(const Dev &D, long long lb, InstState &x, const int *ev, int &n) {
   if (n == 0) return;
-  int base = 0;
-  if (lane_id() == 0) base = atomicAdd(&SS.ev_n, n);
-  base = __shfl_sync(0xffffffffu, base, 0);
-  for (int k = lane_id(); k < n; k += 32) D.ev_id[C.ev_off + base + k] = ev[k];
+  for (int k = lane_id(); k < n; k += 32) D.iev[lb + x.evn + k] = ev[k];
   __syncwarp();
+  x.evn += n;
   n = 0;
 }
 
@@ -106,15 +105,9 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
   for (int q = 0; q < kR; ++q) {
     const int s = q * 32 + (int)lane;
     rem[q] = kDead; rid[q] = 0; tq[q] = 0; fin[q] = 0;
-    if (s < x.run_n) { rem[q] = D.run_rem[lb + s]; rid[q] = D.run_id[lb + s]; }
+    if (s < x.run_n) { rem[q] = D.run_rem[lb + s]; rid[q] = D.run_id[lb + s]; tq[q] = D.run_T[lb + s]; fin[q] = D.run_fin[lb + s]; }
     live[q] = __ballot_sync(0xffffffffu, s < x.run_n);
   }
-#pragma unroll
-  for (int q = 0; q < kR; ++q)
-    if ((live[q] >> lane) & 1u) {
-      tq[q] = D.T[C.traj_off + rid[q]];
-      fin[q] = D.prompt[C.grp_off + grp_of(P, rid[q])] + tq[q];
-    }
   // Arrivals are read through two 32-wide register windows, each refilled with one coalesced
   // load per 32 arrivals: window 6 (id, t_arr) for delivery in B6, window 7 (id, gen, T, prompt)
   // for admission in B7.  Lane k of a window holds arrival base + k.
@@ -221,7 +214,7 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
         int ncomp = 0;
 #pragma unroll
         for (int q = 0; q < kR; ++q) ncomp += __popc(d[q]);
-        if (n_ev + ncomp > kEvBuf) flush_events(D, C, SS, sm.ev, n_ev);
+        if (n_ev + ncomp > kEvBuf) flush_events(D, lb, x, sm.ev, n_ev);
         long long release = 0;
         int before = n_ev;
 #pragma unroll
@@ -417,35 +410,48 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
       if (P.skip) {
         // f1: jump over the whole run of quiet steps in closed form.  With
         // kv0 = kv at the current step start and c1 = k1 kv0 + cn, the j-th quiet boundary is
-        //   b_j = nb + (j-1) c1 + k1 k5n (j-1) j / 2            (Eq 7 with kv growing k5 n per step)
+        //   b_j = nb + g(j-1),  g(x) = c1 x + q1 x (x+1) / 2,  q1 = k1 k5n   (Eq 7, kv growing k5 n per step)
         // and boundary j is quiet iff j <= minrem - 1, kv0 + j k5n <= M, b_j <= t_end and
-        // b_j < next arrival.  m = the largest such j (binary search on the exact int128 b_j).
+        // b_j < next arrival.  m = the largest such j: g is increasing, so x = m - 1 is the floor
+        // root of g(x) = t_lim - nb, estimated in fp64 and then fixed by exact int128 checks.
         int mr = kDead;
 #pragma unroll
         for (int q = 0; q < kR; ++q) mr = min(mr, rem[q]);
         mr = warp_min(mr);
         long long m_hi = (long long)mr - 1;
-        m_hi = min(m_hi, (P.M - x.kv) / k5n);
+        m_hi = min(m_hi, (long long)((unsigned)(P.M - x.kv) / (unsigned)k5n));   // M - kv < 2^30
         const long long t_lim = min(t_end, next_arr - 1);
-        const __int128 kv0 = x.kv, nb0 = x.nb;
-        const __int128 c1 = (__int128)P.k1i * kv0 + cn, q1 = (__int128)P.k1i * k5n;
-        long long lo = 0, hi = max(m_hi, 0LL);
-        while (lo < hi) {                                       // largest j in [0, hi] with b_j <= t_lim
-          const long long mid = (lo + hi + 1) >> 1;
-          const __int128 bj = nb0 + (__int128)(mid - 1) * c1 + q1 * (__int128)((mid - 1) * mid / 2);
-          if (bj <= t_lim) lo = mid; else hi = mid - 1;
+        const __int128 c1 = (__int128)P.k1i * x.kv + cn, q1 = (__int128)P.k1i * k5n;
+        auto g = [&](long long xx) -> __int128 { return c1 * xx + q1 * (((__int128)xx * (xx + 1)) >> 1); };
+        long long m = 0;
+#ifdef SF_SKIP_BSEARCH
+        {                                                       // A/B reference: binary search
+          long long lo = 0, hi = max(m_hi, 0LL);
+          while (lo < hi) {
+            const long long mid = (lo + hi + 1) >> 1;
+            if ((__int128)x.nb + g(mid - 1) <= t_lim) lo = mid; else hi = mid - 1;
+          }
+          m = lo;
         }
-        const long long m = lo;
+#else
+        if (m_hi > 0 && x.nb <= t_lim) {
+          const long long R = t_lim - x.nb;
+          const double A = 0.5 * (double)q1, Bq = (double)c1 + A, Rd = (double)R;
+          const double xe = 2.0 * Rd / (Bq + sqrt(Bq * Bq + 4.0 * A * Rd));   // stable root of A x^2 + Bq x = R
+          long long xx = (long long)fmin(fmax(floor(xe), 0.0), (double)(m_hi - 1));
+          while (xx + 1 <= m_hi - 1 && g(xx + 1) <= R) ++xx;
+          while (xx >= 0 && g(xx) > R) --xx;
+          m = xx + 1;
+        }
+#endif
         if (m > 0) {
 #pragma unroll
           for (int q = 0; q < kR; ++q) rem[q] -= (int)m;
+          x.nb = (long long)((__int128)x.nb + g(m));                 // b_{m+1} = nb + g(m)
           x.kv += m * k5n;
           x.tokens += m * nlive;
           x.iters += m * nlive;
           x.ticks += m;
-          // b_{m+1} = b_m + k1 (kv0 + m k5n) + cn
-          const __int128 bm = nb0 + (__int128)(m - 1) * c1 + q1 * (__int128)((m - 1) * m / 2);
-          x.nb = (long long)(bm + (__int128)P.k1i * (kv0 + (__int128)m * k5n) + cn);
         }
       } else {
         for (;;) {
@@ -466,9 +472,9 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
       }
     }
   }
-  flush_events(D, C, SS, sm.ev, n_ev);
+  flush_events(D, lb, x, sm.ev, n_ev);
 #ifdef SF_CHECK
-  assert(SS.ev_n <= C.cap);
+  assert(x.evn <= C.cap);
   assert(nlive >= 0 && nlive <= 32 * kR && x.wn >= 0 && x.wn <= cap && x.kv >= 0 && x.kv <= P.M);
 #pragma unroll
   for (int q = 0; q < kR; ++q) assert(!((live[q] >> lane) & 1u) || (rem[q] > 0 && rem[q] <= tq[q]));
@@ -481,6 +487,8 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
       const int pos = before + __popc(live[q] & lanemask_lt());
       D.run_rem[lb + pos] = rem[q];
       D.run_id[lb + pos] = rid[q];
+      D.run_T[lb + pos] = tq[q];
+      D.run_fin[lb + pos] = fin[q];
     }
     before += __popc(live[q]);
   }
@@ -512,21 +520,23 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
       long long release = 0;
       for (int base = 0; base < x.run_n; base += 32) {
         const int k = base + (int)lane;
-        int rem = 0, id = 0;
+        int rem = 0, id = 0, Tk = 0, fk = 0;
         bool ab = false;
         if (k < x.run_n) {
-          rem = D.run_rem[lb + k]; id = D.run_id[lb + k];
+          rem = D.run_rem[lb + k]; id = D.run_id[lb + k]; Tk = D.run_T[lb + k]; fk = D.run_fin[lb + k];
           ab = D.loc[C.traj_off + id] == L_ABORTED;
           if (ab) {
-            const int gj = D.T[C.traj_off + id] - rem;
-            release += k5 * (long long)(D.prompt[C.grp_off + grp_of(P, id)] + gj);
-            D.gen[C.traj_off + id] = gj;
+            release += k5 * (long long)(fk - rem);                                   // p + gen
+            D.gen[C.traj_off + id] = Tk - rem;
           }
         }
         const bool keep = k < x.run_n && !ab;
         const unsigned mk = __ballot_sync(0xffffffffu, keep);
         __syncwarp();
-        if (keep) { const int pos = out + __popc(mk & lanemask_lt()); D.run_rem[lb + pos] = rem; D.run_id[lb + pos] = id; }
+        if (keep) {
+          const int pos = out + __popc(mk & lanemask_lt());
+          D.run_rem[lb + pos] = rem; D.run_id[lb + pos] = id; D.run_T[lb + pos] = Tk; D.run_fin[lb + pos] = fk;
+        }
         out += __popc(mk);
         __syncwarp();
       }
@@ -542,16 +552,16 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
       for (int base = 0; base < n0; base += 32) {
         const int k = base + (int)lane;
         const bool valid = k < n0;
-        int rem = 1, id = 0;
-        if (valid) { rem = D.run_rem[lb + k] - 1; id = D.run_id[lb + k]; }
+        int rem = 1, id = 0, Tk = 0, fk = 0;
+        if (valid) { rem = D.run_rem[lb + k] - 1; id = D.run_id[lb + k]; Tk = D.run_T[lb + k]; fk = D.run_fin[lb + k]; }
         const bool done = valid && rem == 0;
         const bool keep = valid && !done;
         const unsigned mk = __ballot_sync(0xffffffffu, keep);
         const unsigned md = __ballot_sync(0xffffffffu, done);
         const int pos = out + __popc(mk & lanemask_lt());
         __syncwarp();
-        if (keep) { D.run_rem[lb + pos] = rem; D.run_id[lb + pos] = id; }
-        if (done) emit_completion(P, D, C, SS, id, b, release);
+        if (keep) { D.run_rem[lb + pos] = rem; D.run_id[lb + pos] = id; D.run_T[lb + pos] = Tk; D.run_fin[lb + pos] = fk; }
+        if (done) emit_completion(D, C, lb, id, Tk, fk, b, x.evn + ncomp + __popc(md & lanemask_lt()), k5, release);
         out += __popc(mk);
         ncomp += __popc(md);
       }
@@ -559,6 +569,7 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
       x.kv += k5 * n0 - release;
       x.tokens += n0;
       x.run_n = out;
+      x.evn += ncomp;
       x.cc += ncomp;
       x.comps += ncomp;
       x.st = I_IDLE;
@@ -569,8 +580,9 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
       const int k = x.run_n - 1;
       const int id = D.run_id[lb + k];
       const long long j = C.traj_off + id;
-      const int g_ = D.T[j] - D.run_rem[lb + k];
-      x.kv -= k5 * (long long)(D.prompt[C.grp_off + grp_of(P, id)] + g_);
+      const int rk = D.run_rem[lb + k];
+      const int g_ = D.run_T[lb + k] - rk;
+      x.kv -= k5 * (long long)(D.run_fin[lb + k] - rk);                         // p + gen
       x.whead = x.whead == 0 ? cap - 1 : x.whead - 1;
       if (lane == 0) {
         D.gen[j] = g_;
@@ -610,8 +622,11 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
       const long long ctx = D.prompt[C.grp_off + grp_of(P, id)] + gj;
       if (x.kv + k5 * ctx > P.M) break;
       if (lane == 0) {
+        const int Tj = D.T[j];
         D.run_id[lb + x.run_n] = id;
-        D.run_rem[lb + x.run_n] = D.T[j] - gj;
+        D.run_rem[lb + x.run_n] = Tj - gj;
+        D.run_T[lb + x.run_n] = Tj;
+        D.run_fin[lb + x.run_n] = (int)(ctx - gj) + Tj;
         D.loc[j] = L_RUN;
       }
       x.kv += k5 * ctx;
@@ -654,7 +669,7 @@ __device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D,
   x.kv = D.ikv[gi]; x.prefill = D.iprefill[gi]; x.cc = D.ic[gi]; x.v = D.iv[gi];
   x.run_n = D.irun_n[gi]; x.whead = D.iwhead[gi]; x.wn = D.iwn[gi];
   x.arr_n = D.iarr_n[gi]; x.arr_head = 0;
-  x.abortn = D.iabort[gi]; x.abortarr = D.iabort_arr[gi];
+  x.abortn = D.iabort[gi]; x.abortarr = D.iabort_arr[gi]; x.evn = D.iev_n[gi];
   x.ticks = x.iters = x.tokens = x.comps = x.preempts = 0;
   // W6: commands to an idle instance apply at a boundary at t
   x.t_cmd = (x.st == I_IDLE && (x.pullpend || x.intkind != INT_NONE || x.abortn > 0)) ? t : kInf;
@@ -680,6 +695,7 @@ __device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D,
     D.ipullpend[gi] = x.pullpend; D.iintkind[gi] = x.intkind;
     D.ikv[gi] = x.kv; D.iprefill[gi] = x.prefill; D.ic[gi] = x.cc; D.iv[gi] = x.v;
     D.irun_n[gi] = x.run_n; D.iwhead[gi] = x.whead; D.iwn[gi] = x.wn; D.iarr_n[gi] = remain;
+    D.iev_n[gi] = x.evn;
     if (x.abortn != D.iabort[gi]) D.iabort[gi] = x.abortn;
     if (x.abortarr != D.iabort_arr[gi]) D.iabort_arr[gi] = x.abortarr;
     metric_add(SS, M_TICKS, x.ticks);

@@ -14,9 +14,12 @@
 
 namespace sf {
 
-constexpr int kCoordWarps = 4; // scenarios per 128-thread block
+#ifndef SF_COORD_WARPS
+#define SF_COORD_WARPS 4
+#endif
+constexpr int kCoordWarps = SF_COORD_WARPS;   // scenarios per block
 #ifndef SF_COORD_MINB
-#define SF_COORD_MINB 4      // blocks per SM for the 1-slot variant: 128 registers, no spills (measured)
+#define SF_COORD_MINB (16 / SF_COORD_WARPS)  // 1-slot variant: 16 warps per SM = 128 registers, no spills (measured)
 #endif
 constexpr int kArrStage = 128; // route records staged per warp in shared memory
 

@@ -14,7 +14,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, SF_ADV_MINB) k_advance(GP
   if (gi >= n_inst_total) return;
   const int s = D.inst_scen[gi];
   if (P.pdl) warp_wait_geq(&D.f_coord[s], P.epoch);     // this scenario's coordinator is done
+  SF_TRACE_AT(4LL * P.n_scen + 2LL * gi);
   advance_instance(P, D, gi, stage_all[threadIdx.x >> 5]);
+  SF_TRACE_AT(4LL * P.n_scen + 2LL * gi + 1);
   __threadfence();                                 // this lane's writes, device-wide
   __syncwarp();
   if ((threadIdx.x & 31) == 0) add_release(&D.f_adv[s], 1);

@@ -5,13 +5,15 @@
 namespace sf {
 
 template <int KS>
-__global__ void __launch_bounds__(128, KS == 1 ? SF_COORD_MINB : 2) k_begin_coord(GParams P, Dev D) {
+__global__ void __launch_bounds__(32 * kCoordWarps, KS == 1 ? SF_COORD_MINB : 8 / kCoordWarps) k_begin_coord(GParams P, Dev D) {
   __shared__ Stage stage_all[kCoordWarps];
   pdl_trigger();                                   // the advance kernel may be scheduled now
   const int s = blockIdx.x * kCoordWarps + (threadIdx.x >> 5);
   if (s >= P.n_scen) return;
   if (P.pdl) warp_wait_geq(&D.f_led[s], P.epoch - 1);   // this scenario's previous window is done
+  SF_TRACE_AT(4LL * s);
   coord_scenario<KS>(P, D, s, stage_all[threadIdx.x >> 5]);
+  SF_TRACE_AT(4LL * s + 1);
   __threadfence();                                 // this lane's writes, device-wide
   __syncwarp();
   if ((threadIdx.x & 31) == 0) st_release(&D.f_coord[s], P.epoch);
@@ -21,7 +23,8 @@ __global__ void __launch_bounds__(128, KS == 1 ? SF_COORD_MINB : 2) k_begin_coor
 
 void sf_launch_begin_coord(const sf::GParams &P, const sf::Dev &D, int n_scen, int max_inst, cudaStream_t st) {
   const int blocks = (n_scen + sf::kCoordWarps - 1) / sf::kCoordWarps;
-  if (max_inst <= 32) sf_launch_pdl(sf::k_begin_coord<1>, blocks, 128, st, P.pdl, P, D);
-  else if (max_inst <= 64) sf_launch_pdl(sf::k_begin_coord<2>, blocks, 128, st, P.pdl, P, D);
-  else sf_launch_pdl(sf::k_begin_coord<4>, blocks, 128, st, P.pdl, P, D);
+  const int thr = 32 * sf::kCoordWarps;
+  if (max_inst <= 32) sf_launch_pdl(sf::k_begin_coord<1>, blocks, thr, st, P.pdl, P, D);
+  else if (max_inst <= 64) sf_launch_pdl(sf::k_begin_coord<2>, blocks, thr, st, P.pdl, P, D);
+  else sf_launch_pdl(sf::k_begin_coord<4>, blocks, thr, st, P.pdl, P, D);
 }

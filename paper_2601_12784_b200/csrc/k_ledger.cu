@@ -10,7 +10,9 @@ __global__ void __launch_bounds__(128) k_ledger(GParams P, Dev D) {
   const int s = blockIdx.x * kLedgerWarps + (threadIdx.x >> 5);
   if (s >= P.n_scen) return;
   if (P.pdl) warp_wait_geq(&D.f_adv[s], P.epoch * D.sc[s].I);   // all its instances advanced
+  SF_TRACE_AT(4LL * s + 2);
   ledger_scenario(P, D, s, stage_all[threadIdx.x >> 5]);
+  SF_TRACE_AT(4LL * s + 3);
   __threadfence();                                 // this lane's writes, device-wide
   __syncwarp();
   if ((threadIdx.x & 31) == 0) st_release(&D.f_led[s], P.epoch);

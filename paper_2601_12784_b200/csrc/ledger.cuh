@@ -178,6 +178,7 @@ struct EvStage {
   long long t[kEvStage];
   int id[kEvStage];
   int srt[kEvStage];
+  int ioff[kMaxInst + 1];         // start of each instance's events in the window's event order
 };
 
 // One window of W8-W9 for scenario s, executed by one warp (es: that warp's staging).
@@ -187,7 +188,36 @@ __device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, 
   ScenState &SS = D.ss[s];
   if (SS.err) return;
   const long long t_end = SS.t + P.delta;
-  const int n = SS.ev_n;
+  // Pending reward events: the carry list D.ev_id[ev_off, ev_off + SS.ev_n) (not yet due in an
+  // earlier window) followed by this window's completions in the instances' segments (D.iev,
+  // written by k_advance without atomics), instance by instance.
+  const int n_carry = SS.ev_n;
+  int n = n_carry;
+  for (int i0 = 0; i0 < C.I; i0 += 32) {
+    const int i = i0 + (int)lane;
+    const int ni = i < C.I ? D.iev_n[C.inst_off + i] : 0;
+    const int off = n + warp_excl_scan(ni);
+    if (i < C.I) es.ioff[i] = off;
+    n = __shfl_sync(0xffffffffu, off + ni, 31);
+  }
+  if (lane == 0) es.ioff[C.I] = n;
+  __syncwarp();
+  auto seg_of = [&](int e) {                      // instance whose segment holds event e >= n_carry
+    int lo = 0, hi = C.I - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (es.ioff[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+  };
+  if (n > kEvStage) {                             // rare: gather the segments into the carry list
+    for (int e = n_carry + (int)lane; e < n; e += 32) {
+      const int i = seg_of(e);
+      D.ev_id[C.ev_off + e] = D.iev[C.list_off + (long long)i * C.cap + (e - es.ioff[i])];
+    }
+    __syncwarp();
+  }
+  for (int i = lane; i < C.I; i += 32) D.iev_n[C.inst_off + i] = 0;
 #ifdef SF_CHECK
   assert(n >= 0 && n <= C.cap);
 #endif
@@ -199,7 +229,9 @@ __device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, 
   if (n <= kEvStage) {
     // stage (t_complete, id), rank-sort by (t_reward, id) (W8) in shared memory
     for (int e = lane; e < n; e += 32) {
-      const int id = D.ev_id[C.ev_off + e];
+      int id;
+      if (e < n_carry) id = D.ev_id[C.ev_off + e];
+      else { const int i = seg_of(e); id = D.iev[C.list_off + (long long)i * C.cap + (e - es.ioff[i])]; }
       es.id[e] = id;
       es.t[e] = D.t_complete[C.traj_off + id];
     }

@@ -253,6 +253,8 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
        dalloc(c, &D.iuntil, inst, 0) && dalloc(c, &D.iprefill, inst, 0) && dalloc(c, &D.iabort, inst, 0) &&
        dalloc(c, &D.iabort_arr, inst, 0) &&
        dalloc(c, &D.f_coord, ns, 0) && dalloc(c, &D.f_adv, ns, 0) && dalloc(c, &D.f_led, ns, 0);
+  ok = ok && dalloc(c, &D.run_T, list, 0) && dalloc(c, &D.run_fin, list, 0) && dalloc(c, &D.iev, list, 0) &&
+       dalloc(c, &D.iev_n, inst, 0);
   ok = ok && dalloc(c, &D.run_id, list, 0) && dalloc(c, &D.run_rem, list, 0) && dalloc(c, &D.wait_id, list, 0) &&
        dalloc(c, &D.arr_id, list, 0) && dalloc(c, &D.arr_t, list, 0);
   ok = ok && dalloc(c, &D.led_st, led, 0) && dalloc(c, &D.led_g, led, 0xFF) && dalloc(c, &D.led_v, led, 0xFF) &&
@@ -269,6 +271,11 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
 #else
   D.dbg = nullptr;
   D.dbg2 = nullptr;
+#endif
+#ifdef SF_TRACE
+  ok = ok && dalloc(c, &D.trace, 4LL * ns + 2LL * inst, 0);
+#else
+  D.trace = nullptr;
 #endif
   D.sc = dsc;
   D.ss = dss;
@@ -646,6 +653,14 @@ sf_status sf_debug_coord_cycles(sf_ctx *c, int64_t *out) {
 sf_status sf_debug_adv_cycles(sf_ctx *c, int64_t *out) {
   if (!c || !c->D.dbg2) return SF_E_INVALID;
   cudaMemcpy(out, c->D.dbg2, 8 * sizeof(long long) * c->n_inst_total, cudaMemcpyDeviceToHost);
+  return SF_OK;
+}
+#endif
+
+#ifdef SF_TRACE
+sf_status sf_debug_trace(sf_ctx *c, int64_t *out) {
+  if (!c || !c->D.trace) return SF_E_INVALID;
+  cudaMemcpy(out, c->D.trace, sizeof(long long) * (4LL * c->n_scen + 2LL * c->n_inst_total), cudaMemcpyDeviceToHost);
   return SF_OK;
 }
 #endif

@@ -57,10 +57,12 @@ _lib = None
 
 
 def load_library(path: str = LIB_PATH):
-    """Load libstaleflow.so (built by paper_2601_12784_b200/build.py); raises if absent."""
+    """Load libstaleflow.so (built by paper_2601_12784_b200/build.py); raises if absent.
+    SF_LIB overrides the path (A/B experiments between two builds of this library)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("SF_LIB", path)
     if not os.path.exists(path):
         raise RuntimeError(f"{path} not built: run `python -m paper_2601_12784_b200.build` "
                            "(there is no CPU fallback)")
