@@ -27,6 +27,8 @@ struct sf_ctx {
   int max_inst = 1;
   int fused = 0;                      // launch mode: 1 = one fused window kernel (k_window)
   int pdl = 1;                        // programmatic dependent launch between window kernels
+  int dyn = 1;                        // dataflow window kernel (k_dyn.cu)
+  int dyn_blocks = 0;
   long long epoch = 0;                // split-mode windows launched (PDL flag targets)
   int n_scen = 0;
   int device = 0;
@@ -216,9 +218,11 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
     bits += bwords; mlq += 3LL * S.cap + 2; ev += S.cap; batch += batch_rec; cmd += 4LL * P.cmdlog_cap;
   }
   c->n_inst_total = (int)inst;
-  // launch mode: the three-kernel path by default (measured faster on C5);
-  // SF_LAUNCH=fused selects the fused per-scenario window kernel (tests run both)
+  // launch mode: three kernels per window with programmatic dependent launch by
+  // default (SF_PDL=0: serialized); SF_LAUNCH=dyn the dataflow window kernel, SF_LAUNCH=fused the
+  // fused per-scenario window kernel (tests run every mode)
   c->fused = 0;
+  c->dyn = 0;
   // decode-step mode: closed-form skipping of quiet steps by default;
   // SF_ADVANCE=step processes every decode step individually (tests run both)
   c->P.skip = 1;
@@ -229,8 +233,9 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
   c->P.epoch = 0;
   if (const char *m = getenv("SF_ADVANCE")) c->P.skip = strcmp(m, "step") != 0;
   if (const char *m = getenv("SF_LAUNCH")) {
-    if (!strcmp(m, "split")) c->fused = 0;
-    if (!strcmp(m, "fused")) c->fused = c->max_inst <= 32;
+    if (!strcmp(m, "split")) { c->fused = 0; c->dyn = 0; }
+    if (!strcmp(m, "fused")) { c->fused = c->max_inst <= 32; c->dyn = 0; }
+    if (!strcmp(m, "dyn")) { c->fused = 0; c->dyn = 1; }
   }
   const long long ntraj = (long long)ns * pool_traj, ngrp = (long long)ns * P.pool_cap;
   Dev &D = c->D;
@@ -252,7 +257,13 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
        dalloc(c, &D.iacc, inst, 0) && dalloc(c, &D.ikv, inst, 0) && dalloc(c, &D.inb, inst, 0) &&
        dalloc(c, &D.iuntil, inst, 0) && dalloc(c, &D.iprefill, inst, 0) && dalloc(c, &D.iabort, inst, 0) &&
        dalloc(c, &D.iabort_arr, inst, 0) &&
-       dalloc(c, &D.f_coord, ns, 0) && dalloc(c, &D.f_adv, ns, 0) && dalloc(c, &D.f_led, ns, 0);
+       dalloc(c, &D.f_coord, ns, 0) && dalloc(c, &D.f_adv, ns, 0) && dalloc(c, &D.f_led, ns, 0) &&
+       dalloc(c, &D.q_ctr, 4 + (long long)ns + inst + ns, 0);
+  if (ok) {
+    D.q_done = D.q_ctr + 4;
+    D.q_tasks = D.q_done + ns;
+    D.q_total = (int)(inst + ns);
+  }
   ok = ok && dalloc(c, &D.run_T, list, 0) && dalloc(c, &D.run_fin, list, 0) && dalloc(c, &D.iev, list, 0) &&
        dalloc(c, &D.iev_n, inst, 0);
   ok = ok && dalloc(c, &D.run_id, list, 0) && dalloc(c, &D.run_rem, list, 0) && dalloc(c, &D.wait_id, list, 0) &&
@@ -379,7 +390,20 @@ sf_status sf_step(sf_ctx *c, int32_t n_windows, sf_step_stats *out) {
   // scenario's advance starts when ITS coordinator is done instead of after the slowest one.
   // Profiling (events between kernels) serializes the launches.
   const int pdl = c->pdl && !c->prof_on;
-  for (int w = 0; w < (c->fused ? 0 : n_windows); ++w) {
+  const bool dyn = c->dyn && !c->fused && !c->prof_on;   // profiling attributes time per kernel: split
+  if (dyn && n_windows > 0) {
+    if (c->dyn_blocks == 0) c->dyn_blocks = sf_dyn_blocks(c->max_inst);
+    const size_t qbytes = sizeof(int) * (4 + (size_t)c->n_scen + (size_t)c->D.q_total);
+    for (int w = 0; w < n_windows; ++w) {
+      GParams P = c->P;
+      P.epoch = ++c->epoch;
+      P.pdl = 0;
+      if (!cuda_ok(c, cudaMemsetAsync(c->D.q_ctr, 0, qbytes, c->stream), "queue reset")) return SF_E_CUDA;
+      sf_launch_window_dyn(P, c->D, c->n_scen, c->max_inst, c->dyn_blocks, c->stream);
+      c->launches += 1;
+    }
+  }
+  for (int w = 0; w < (c->fused || dyn ? 0 : n_windows); ++w) {
     GParams P = c->P;
     P.epoch = ++c->epoch;
     P.pdl = pdl && w > 0;                 // the first coordinator follows arbitrary stream work

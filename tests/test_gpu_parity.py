@@ -16,14 +16,16 @@ from tests.parity import compare, make_pair, run_lockstep, submit_both
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["auto", "fused", "step", "nopdl"])
+@pytest.fixture(params=["auto", "fused", "step", "dyn", "nopdl"])
 def launch_mode(request, monkeypatch):
     """Every launch / decode-step mode must give identical results: default (three kernels with
     programmatic dependent launch, closed-form quiet steps), fused window kernel, one-by-one
-    decode steps, and three fully serialized kernels."""
+    decode steps, the dataflow window kernel, and three fully serialized kernels."""
     monkeypatch.delenv("SF_LAUNCH", raising=False)
     monkeypatch.delenv("SF_ADVANCE", raising=False)
     monkeypatch.delenv("SF_PDL", raising=False)
+    if request.param == "dyn":
+        monkeypatch.setenv("SF_LAUNCH", "dyn")
     if request.param == "nopdl":
         monkeypatch.setenv("SF_PDL", "0")
     if request.param == "fused":
