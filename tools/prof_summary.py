@@ -1,0 +1,69 @@
+"""Summarise gpurun_out/prof (tools/profile_round.sh) into profiles/<round>/ and refresh
+profiles/ncu_traffic.json (dram bytes per launch of each window kernel, read by bench.py)."""
+import collections, csv, json, os, subprocess, sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+src = os.path.join(ROOT, "gpurun_out", "prof")
+dst = os.path.join(ROOT, "profiles", sys.argv[1] if len(sys.argv) > 1 else "r01b")
+os.makedirs(dst, exist_ok=True)
+
+# launch list -> per-kernel totals over the timed steps of the command
+lines = [l for l in open(os.path.join(src, "launches.csv")) if l.startswith('"')]
+rows = list(csv.reader(lines))
+h = rows[0]
+ki, vi, mi = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Name")
+tot = collections.OrderedDict()
+for r in rows[1:]:
+    if r[mi] != "gpu__time_duration.sum":
+        continue
+    name = r[ki].split("(")[0]
+    t = tot.setdefault(name, [0, 0.0])
+    t[0] += 1
+    t[1] += float(r[vi]) / 1e3
+win = {k: v for k, v in tot.items() if any(x in k for x in ("k_begin_coord", "k_advance", "k_ledger"))}
+s = sum(v[1] for v in win.values()) or 1.0
+with open(os.path.join(dst, "launch_summary.csv"), "w") as f:
+    f.write("# ncu launch list (gpu__time_duration.sum, --clock-control none, cold-cache serialised)\n")
+    f.write("# command: python bench.py --profile-run --steps 3 --warmup 60 (C5, 4096 scenarios; incl. the replay context)\n")
+    f.write("kernel,launches,total_us,avg_us,share_of_window_kernels\n")
+    for k, (n, us) in sorted(tot.items(), key=lambda kv: -kv[1][1]):
+        f.write(f"{k},{n},{us:.1f},{us / n:.1f},{(us / s if k in win else 0):.3f}\n")
+
+# full capture -> key metrics per kernel
+raw = list(csv.reader(open(os.path.join(src, "full_raw.csv"))))
+hdr, units = raw[0], raw[1]
+want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread", "smsp__average_warp_latency_per_inst_issued.ratio",
+        "sm__inst_executed.avg.per_cycle_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "lts__t_sector_hit_rate.pct", "launch__grid_size", "launch__occupancy_limit_registers"]
+out, traffic = {}, {}
+kn = hdr.index("Kernel Name")
+for r in raw[2:]:
+    name = r[kn].split("(")[0]
+    d = {}
+    for w in want:
+        if w in hdr:
+            i = hdr.index(w)
+            d[w] = f"{r[i]} {units[i]}".strip()
+    out[name] = d
+    rd = float(r[hdr.index("dram__bytes_read.sum")]) * (1e6 if units[hdr.index("dram__bytes_read.sum")] == "Mbyte" else 1e3 if units[hdr.index("dram__bytes_read.sum")] == "Kbyte" else 1)
+    wr = float(r[hdr.index("dram__bytes_write.sum")]) * (1e6 if units[hdr.index("dram__bytes_write.sum")] == "Mbyte" else 1e3 if units[hdr.index("dram__bytes_write.sum")] == "Kbyte" else 1)
+    traffic[name] = rd + wr
+json.dump(out, open(os.path.join(dst, "ncu_kernels.json"), "w"), indent=1)
+json.dump({"source": f"profiles/{os.path.basename(dst)}/ncu_kernels.json (ncu --set full, window 60 of the C5 bench workload)",
+           "dram_bytes_per_launch": traffic}, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
+
+# details page per kernel + hot source lines
+det = list(csv.reader(open(os.path.join(src, "full_details.csv"))))
+dh = det[0]
+for name in out:
+    short = name.split()[-1].split("<")[0]
+    with open(os.path.join(dst, f"{short}_details.txt"), "w") as f:
+        for r in det[1:]:
+            if r[dh.index("Kernel Name")].split("(")[0] == name:
+                f.write(f"{r[dh.index('Section Name')]:<40} {r[dh.index('Metric Name')]:<50} {r[dh.index('Metric Unit')]:<12} {r[dh.index('Metric Value')]}\n")
+subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), os.path.join(src, "full_src.csv"), "40"],
+               stdout=open(os.path.join(dst, "window_kernels_lines.txt"), "w"))
+print(open(os.path.join(dst, "launch_summary.csv")).read())
+print(json.dumps(traffic, indent=1))
