@@ -12,7 +12,11 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libstaleflow.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"]
+# -dlcm=cg: global loads are cached in L2 only.  With programmatic dependent launch the window
+# kernels run concurrently and hand data over per scenario through release/acquire flags; an
+# L1-cached load could return a line filled with pre-release data by another warp of the SM
+# (measured: an SF_CHECK build diverged under PDL, bit-exact with L1 bypassed).
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-dlcm=cg", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"]
 FLAGS += [f for f in os.environ.get("SF_NVCC_EXTRA", "").split() if f]
 
 

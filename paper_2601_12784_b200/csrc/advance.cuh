@@ -473,7 +473,7 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
     }
   }
   flush_events(D, lb, x, sm.ev, n_ev);
-#ifdef SF_CHECK
+#ifdef SF_CHECK_ADV
   assert(x.evn <= C.cap);
   assert(nlive >= 0 && nlive <= 32 * kR && x.wn >= 0 && x.wn <= cap && x.kv >= 0 && x.kv <= P.M);
 #pragma unroll

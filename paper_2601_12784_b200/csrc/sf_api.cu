@@ -27,6 +27,7 @@ struct sf_ctx {
   int max_inst = 1;
   int fused = 0;                      // launch mode: 1 = one fused window kernel (k_window)
   int pdl = 1;                        // programmatic dependent launch between window kernels
+  int pdl_mask = 0;                   // debugging (SF_PDL_MASK): bit 0 serializes the advance, bit 1 the ledger
   int dyn = 1;                        // dataflow window kernel (k_dyn.cu)
   int dyn_blocks = 0;
   long long epoch = 0;                // split-mode windows launched (PDL flag targets)
@@ -229,6 +230,7 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
   // programmatic dependent launch between the window kernels; SF_PDL=0 disables
   c->pdl = 1;
   if (const char *m = getenv("SF_PDL")) c->pdl = strcmp(m, "0") != 0;
+  if (const char *m = getenv("SF_PDL_MASK")) c->pdl_mask = atoi(m);
   c->P.pdl = 0;
   c->P.epoch = 0;
   if (const char *m = getenv("SF_ADVANCE")) c->P.skip = strcmp(m, "step") != 0;
@@ -410,10 +412,11 @@ sf_status sf_step(sf_ctx *c, int32_t n_windows, sf_step_stats *out) {
     prof_mark(c, 0);
     sf_launch_begin_coord(P, c->D, c->n_scen, c->max_inst, c->stream);
     prof_mark(c, 0);
-    P.pdl = pdl;
+    P.pdl = pdl && !(c->pdl_mask & 1);
     prof_mark(c, 1);
     sf_launch_advance(P, c->D, c->n_inst_total, c->stream);
     prof_mark(c, 1);
+    P.pdl = pdl && !(c->pdl_mask & 2);
     prof_mark(c, 2);
     sf_launch_ledger(P, c->D, c->n_scen, c->stream);
     prof_mark(c, 2);
@@ -677,6 +680,30 @@ sf_status sf_debug_coord_cycles(sf_ctx *c, int64_t *out) {
 sf_status sf_debug_adv_cycles(sf_ctx *c, int64_t *out) {
   if (!c || !c->D.dbg2) return SF_E_INVALID;
   cudaMemcpy(out, c->D.dbg2, 8 * sizeof(long long) * c->n_inst_total, cudaMemcpyDeviceToHost);
+  return SF_OK;
+}
+#endif
+
+#ifdef SF_CHECK
+// SF_CHECK builds: raw ledger ring of one scenario as (state, group, version) triples, then the
+// per-buffer reserved / occupied counts, then ScenState.cu.
+sf_status sf_debug_ledger(sf_ctx *c, int32_t scen, int64_t *out) {
+  if (!c || scen < 0 || scen >= c->n_scen) return SF_E_INVALID;
+  const ScenConst &S = c->hsc[scen];
+  const int nslot = (S.eta + 1) * c->P.B;
+  std::vector<uint8_t> st(nslot);
+  std::vector<int> g(nslot), v(nslot), nres(S.eta + 1), nocc(S.eta + 1);
+  ScenState ss;
+  cudaMemcpy(st.data(), c->D.led_st + S.led_off, nslot, cudaMemcpyDeviceToHost);
+  cudaMemcpy(g.data(), c->D.led_g + S.led_off, 4 * nslot, cudaMemcpyDeviceToHost);
+  cudaMemcpy(v.data(), c->D.led_v + S.led_off, 4 * nslot, cudaMemcpyDeviceToHost);
+  cudaMemcpy(nres.data(), c->D.led_nres + S.ring_off, 4 * (S.eta + 1), cudaMemcpyDeviceToHost);
+  cudaMemcpy(nocc.data(), c->D.led_nocc + S.ring_off, 4 * (S.eta + 1), cudaMemcpyDeviceToHost);
+  cudaMemcpy(&ss, c->D.ss + scen, sizeof(ScenState), cudaMemcpyDeviceToHost);
+  long long k = 0;
+  for (int i = 0; i < nslot; ++i) { out[k++] = st[i]; out[k++] = g[i]; out[k++] = v[i]; }
+  for (int i = 0; i <= S.eta; ++i) { out[k++] = nres[i]; out[k++] = nocc[i]; }
+  out[k++] = ss.cu;
   return SF_OK;
 }
 #endif

@@ -1,5 +1,5 @@
 # ncu source-level capture of one heavy-window coordinator launch (window ~95 of the C5 bench).
-SF_NVCC_EXTRA="-DSF_COORD_MINB=4" python -m paper_2601_12784_b200.build --force > /dev/null
+python -m paper_2601_12784_b200.build > /dev/null
 python bench.py --profile-run --steps 100 > /dev/null 2>&1 || exit 1
 ncu --set full --import-source on --clock-control none -k regex:k_begin_coord --launch-skip ${SKIP:-94} --launch-count 1 \
   -o gpurun_out/coord_heavy -f python bench.py --profile-run --steps 100 > gpurun_out/ncu_coord.log 2>&1
