@@ -872,13 +872,22 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
       const int bw = (P.B + 31) >> 5;
       c.use_bits = nring * bw <= kEmptyWords;
       if (c.use_bits) {
-        for (int r = 0; r < nring; ++r)
-          for (int w = 0; w < bw; ++w) {
-            const int sl = w * 32 + (int)lane;
-            const bool e = sl < P.B && D.led_st[C.led_off + (long long)r * P.B + sl] == E_EMPTY;
-            const unsigned m = __ballot_sync(0xffffffffu, e);
-            if (lane == 0) sg.empty[r * bw + w] = m;
+        // 8 words per round: all slot loads of a round are issued before its ballots, so a small
+        // ledger costs one memory round trip instead of one per 32 slots
+        const int nw = nring * bw;
+        for (int w0 = 0; w0 < nw; w0 += 8) {
+          bool e[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int w = w0 + u, r = w / bw, sl = (w - r * bw) * 32 + (int)lane;
+            e[u] = w < nw && sl < P.B && D.led_st[C.led_off + (long long)r * P.B + sl] == E_EMPTY;
           }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const unsigned m = __ballot_sync(0xffffffffu, e[u]);
+            if (lane == 0 && w0 + u < nw) sg.empty[w0 + u] = m;
+          }
+        }
       }
     }
     __syncwarp();

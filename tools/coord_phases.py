@@ -23,3 +23,8 @@ for w in range(100):
 a = np.concatenate(rows)
 print("cols: total routes ck0(pre-sync) ck1(sync) ck2(migr) ck3(mlq2) ck4(route) ck5(arrivals) window scen")
 for t in np.argsort(-a[:, 0])[:12]: print(a[t].tolist(), "eta", p.scenarios[a[t, 9]].eta)
+# typical scenario: median cycles of each phase over all scenario-windows
+ph = np.diff(np.concatenate([np.zeros((len(a), 1)), a[:, 2:8]], 1), axis=1)   # ck0, ck1-ck0, ..., ck5-ck4
+tot = a[:, 0]
+print("median total %.0f; median per phase [pre-sync, sync, migr, mlq2, route, arrivals]:" % np.median(tot),
+      np.median(ph, 0).round(0).tolist(), "post (total - ck5):", np.median(tot - a[:, 7]))
