@@ -70,23 +70,47 @@ __global__ void k_filter(GParams P, Dev D, int s, int g, int *out) {
   }
 }
 
-// Sum of per-scenario metric vectors (integer, order independent) -> out[kMetrics].
-__global__ void k_reduce_metrics(Dev D, int n_scen, long long *out) {
-  __shared__ unsigned long long acc[kMetrics];
-  if (threadIdx.x < kMetrics) acc[threadIdx.x] = 0;
-  __syncthreads();
-  for (int s = threadIdx.x >> 5; s < n_scen; s += blockDim.x >> 5) {
+// Sum of per-scenario metric vectors (integer, order independent; slot 30 is a maximum) ->
+// out[kMetrics].  Grid-wide: lane k of every warp accumulates metric k of a strided set of
+// scenarios in a register (one coalesced 256-byte row per scenario), the warps of a block are
+// combined in shared memory, and the last block to finish adds the per-block partials.
+constexpr int kRedWarps = 8;
+__global__ void __launch_bounds__(32 * kRedWarps) k_reduce_metrics(Dev D, int n_scen, long long *out) {
+  __shared__ unsigned long long acc[kRedWarps][kMetrics];
+  __shared__ bool last;
+  const int warp = threadIdx.x >> 5, k = threadIdx.x & 31;
+  const bool is_max = k == M_MAX_T;
+  unsigned long long v = 0;
+  for (int s = blockIdx.x * kRedWarps + warp; s < n_scen; s += gridDim.x * kRedWarps) {
     const ScenState &SS = D.ss[s];
-    const int k = threadIdx.x & 31;
-    unsigned long long v = SS.m[k];
-    if (k == M_CMD_HASH) v = SS.cmd_hash;
-    if (k == M_SIM_TIME) v = (unsigned long long)SS.t;
-    if (k == M_ERR_SCEN) v = SS.err != 0;
-    if (k == M_MAX_T) atomicMax(&acc[k], (unsigned long long)SS.t);
-    else atomicAdd(&acc[k], v);
+    unsigned long long x = SS.m[k];
+    if (k == M_CMD_HASH) x = SS.cmd_hash;
+    if (k == M_SIM_TIME || k == M_MAX_T) x = (unsigned long long)SS.t;
+    if (k == M_ERR_SCEN) x = SS.err != 0;
+    v = is_max ? max(v, x) : v + x;
+  }
+  acc[warp][k] = v;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long t = 0;
+#pragma unroll
+    for (int w = 0; w < kRedWarps; ++w) t = is_max ? max(t, acc[w][k]) : t + acc[w][k];
+    D.red_part[blockIdx.x * kMetrics + k] = t;
+    __threadfence();
   }
   __syncthreads();
-  if (threadIdx.x < kMetrics) out[threadIdx.x] = (long long)acc[threadIdx.x];
+  if (threadIdx.x == 0) last = atomicAdd(D.red_ctr, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last && warp == 0) {
+    __threadfence();
+    unsigned long long t = 0;
+    for (int b = 0; b < (int)gridDim.x; ++b) {
+      const unsigned long long x = D.red_part[b * kMetrics + k];
+      t = is_max ? max(t, x) : t + x;
+    }
+    out[k] = (long long)t;
+    if (k == 0) *D.red_ctr = 0;                    // ready for the next reduction on the stream
+  }
 }
 
 // 13 int64 per trajectory (include/staleflow.h sf_dump_lifecycles)
@@ -125,16 +149,34 @@ __global__ void k_dump_instances(GParams P, Dev D, int s, long long *out) {
   }
 }
 
-// desc[4k..4k+3] = (scenario, first group, n_groups, source group offset)
-__global__ void k_scatter_pool(Dev D, int G, const int *desc, int n_desc, const int *prompt, const int *target) {
+// desc[4k..4k+3] = (scenario, first group, n_groups, source group offset).  Copies the groups into
+// the pools and validates them on the way (prompt >= 0, 1 <= T <= lim - prompt with lim = M / k5,
+// reading A27): *bad != 0 afterwards if any entry is invalid.  The pool counts are committed
+// separately (k_commit_pool), only for a valid submission.
+__global__ void k_scatter_pool(Dev D, int G, const int *desc, int n_desc, const int *prompt, const int *target, int lim,
+                               int *bad) {
   const int k = blockIdx.x;
   if (k >= n_desc) return;
   const int s = desc[4 * k], g0 = desc[4 * k + 1], ng = desc[4 * k + 2], src = desc[4 * k + 3];
   const ScenConst C = D.sc[s];
-  for (int a = threadIdx.x; a < ng; a += blockDim.x) D.prompt[C.grp_off + g0 + a] = prompt[src + a];
-  for (long long a = threadIdx.x; a < (long long)ng * G; a += blockDim.x)
-    D.T[C.traj_off + (long long)g0 * G + a] = target[(long long)src * G + a];
-  if (threadIdx.x == 0) D.ss[s].n_pool = g0 + ng;
+  int b = 0;
+  for (int a = threadIdx.x; a < ng; a += blockDim.x) {
+    const int p = prompt[src + a];
+    b |= p < 0;
+    D.prompt[C.grp_off + g0 + a] = p;
+  }
+  for (long long a = threadIdx.x; a < (long long)ng * G; a += blockDim.x) {
+    const int T = target[(long long)src * G + a];
+    const int p = prompt[src + a / G];
+    b |= (T < 1) | (T > lim - p);
+    D.T[C.traj_off + (long long)g0 * G + a] = T;
+  }
+  if (__syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
+__global__ void k_commit_pool(Dev D, const int *desc, int n_desc) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_desc; k += gridDim.x * blockDim.x)
+    D.ss[desc[4 * k]].n_pool = desc[4 * k + 1] + desc[4 * k + 2];
 }
 
 }  // namespace sf
@@ -149,7 +191,9 @@ void sf_launch_filter(const sf::GParams &P, const sf::Dev &D, int scen, int grou
   sf::k_filter<<<1, 32, 0, st>>>(P, D, scen, group, out_dev);
 }
 void sf_launch_reduce_metrics(const sf::Dev &D, int n_scen, long long *out_dev, cudaStream_t st) {
-  sf::k_reduce_metrics<<<1, 1024, 0, st>>>(D, n_scen, out_dev);
+  int blocks = (n_scen + 4 * sf::kRedWarps - 1) / (4 * sf::kRedWarps);     // >= 4 scenarios per warp
+  blocks = blocks < 1 ? 1 : (blocks > sf::kRedBlocksMax ? sf::kRedBlocksMax : blocks);
+  sf::k_reduce_metrics<<<blocks, 32 * sf::kRedWarps, 0, st>>>(D, n_scen, out_dev);
 }
 void sf_launch_dump_lifecycles(const sf::GParams &P, const sf::Dev &D, int scen, long long n_traj,
                                long long *out_dev, cudaStream_t st) {
@@ -164,6 +208,9 @@ void sf_launch_dump_instances(const sf::GParams &P, const sf::Dev &D, int scen, 
   sf::k_dump_instances<<<1, 128, 0, st>>>(P, D, scen, out_dev);
 }
 void sf_launch_scatter_pool(const sf::Dev &D, int G, const int *desc_dev, int n_desc, const int *prompt_dev,
-                            const int *target_dev, cudaStream_t st) {
-  if (n_desc > 0) sf::k_scatter_pool<<<n_desc, 256, 0, st>>>(D, G, desc_dev, n_desc, prompt_dev, target_dev);
+                            const int *target_dev, int lim, int *bad_dev, cudaStream_t st) {
+  if (n_desc > 0) sf::k_scatter_pool<<<n_desc, 256, 0, st>>>(D, G, desc_dev, n_desc, prompt_dev, target_dev, lim, bad_dev);
+}
+void sf_launch_commit_pool(const sf::Dev &D, const int *desc_dev, int n_desc, cudaStream_t st) {
+  if (n_desc > 0) sf::k_commit_pool<<<(n_desc + 255) / 256, 256, 0, st>>>(D, desc_dev, n_desc);
 }

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <new>
 #include <string>
@@ -42,6 +43,9 @@ struct sf_ctx {
   int *d_collect = nullptr;
   int *d_stage = nullptr;
   size_t stage_cap = 0;
+  int *h_desc = nullptr;              // pinned staging of submit descriptors
+  size_t h_desc_cap = 0;
+  std::vector<int> pool_tmp;
   long long *d_dump = nullptr;
   size_t dump_cap = 0;
   // live per-kernel timing (sf_profile): CUDA events recorded around every window kernel
@@ -260,7 +264,8 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
        dalloc(c, &D.iuntil, inst, 0) && dalloc(c, &D.iprefill, inst, 0) && dalloc(c, &D.iabort, inst, 0) &&
        dalloc(c, &D.iabort_arr, inst, 0) &&
        dalloc(c, &D.f_coord, ns, 0) && dalloc(c, &D.f_adv, ns, 0) && dalloc(c, &D.f_led, ns, 0) &&
-       dalloc(c, &D.q_ctr, 4 + (long long)ns + inst + ns, 0);
+       dalloc(c, &D.q_ctr, 4 + (long long)ns + inst + ns, 0) &&
+       dalloc(c, &D.red_part, (long long)sf::kRedBlocksMax * sf::kMetrics, 0) && dalloc(c, &D.red_ctr, 1, 0);
   if (ok) {
     D.q_done = D.q_ctr + 4;
     D.q_tasks = D.q_done + ns;
@@ -274,7 +279,7 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
        dalloc(c, &D.led_nres, ring, 0) && dalloc(c, &D.led_nocc, ring, 0);
   ok = ok && dalloc(c, &D.ev_t, 1, 0) && dalloc(c, &D.ev_id, ev, 0) && dalloc(c, &D.tsv_bits, bits, 0) &&
        dalloc(c, &D.mlq, mlq, 0) && dalloc(c, &D.batches, batch, 0) && dalloc(c, &D.cmdlog, cmd, 0);
-  ok = ok && dalloc(c, &c->d_metrics, sf::kMetrics, 0) && dalloc(c, &c->d_collect, 2 + 2 * P.Br, 0);
+  ok = ok && dalloc(c, &c->d_metrics, 2 * sf::kMetrics, 0) && dalloc(c, &c->d_collect, 2 + 2 * P.Br, 0);
   if (!ok) {
     sf_destroy(c);
     return SF_E_NOMEM;
@@ -318,6 +323,7 @@ void sf_destroy(sf_ctx *c) {
   for (void *p : c->allocs) cudaFree(p);
   if (c->d_stage) cudaFree(c->d_stage);
   if (c->d_dump) cudaFree(c->d_dump);
+  if (c->h_desc) cudaFreeHost(c->h_desc);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   delete c;
 }
@@ -329,43 +335,70 @@ sf_status sf_submit_prompts_many(sf_ctx *c, int32_t n, const int32_t *scen_ids, 
   DevGuard dg(c->device);
   if (n < 0 || (n > 0 && (!scen_ids || !n_groups || !prompt || !target))) return fail(c, SF_E_INVALID, "null argument");
   const int G = c->P.G;
-  std::vector<int> desc;
-  std::vector<int> pool = c->hn_pool;
+  // descriptors and capacity checks on the host; the per-element validation (A27) runs inside the
+  // scatter kernel, and the pool counts are committed only if it found nothing invalid
+  if ((size_t)4 * n > c->h_desc_cap) {
+    if (c->h_desc) cudaFreeHost(c->h_desc);
+    c->h_desc = nullptr;
+    c->h_desc_cap = 0;
+    if (cudaMallocHost(&c->h_desc, sizeof(int) * 4 * (size_t)n + sizeof(int)) != cudaSuccess)
+      return fail(c, SF_E_NOMEM, "pinned staging alloc");
+    c->h_desc_cap = 4 * (size_t)n;
+  }
+  int *desc = c->h_desc;
+  std::vector<int> &pool = c->pool_tmp;
+  pool = c->hn_pool;
   long long tot = 0;
   for (int k = 0; k < n; ++k) {
     const int s = scen_ids[k], ng = n_groups[k];
     if (s < 0 || s >= c->n_scen) return fail(c, SF_E_RANGE, "scenario index out of range");
     if (ng < 0 || pool[s] + ng > c->P.pool_cap) return fail(c, SF_E_RANGE, "pool capacity exceeded");
-    for (long long a = 0; a < ng; ++a) {
-      const long long p = prompt[tot + a];
-      if (p < 0) return fail(c, SF_E_INVALID, "negative prompt length");
-      for (int m = 0; m < G; ++m) {
-        const long long T = target[(tot + a) * G + m];
-        if (T < 1 || (long long)c->P.k5 * (p + T) > c->P.M) return fail(c, SF_E_INVALID, "target < 1 or k5*(p+T) > M (A27)");
-      }
-    }
-    desc.push_back(s); desc.push_back(pool[s]); desc.push_back(ng); desc.push_back((int)tot);
+    desc[4 * k] = s; desc[4 * k + 1] = pool[s]; desc[4 * k + 2] = ng; desc[4 * k + 3] = (int)tot;
     pool[s] += ng;
     tot += ng;
   }
   if (tot == 0) return SF_OK;
-  const size_t need = (size_t)desc.size() + (size_t)tot + (size_t)tot * G;
+  const size_t nd = 4 * (size_t)n;
+  const size_t need = 1 + nd + (size_t)tot + (size_t)tot * G;
   if (need > c->stage_cap) {
     if (c->d_stage) cudaFree(c->d_stage);
     c->d_stage = nullptr;
     if (cudaMalloc(&c->d_stage, need * sizeof(int)) != cudaSuccess) return fail(c, SF_E_NOMEM, "staging alloc");
     c->stage_cap = need;
   }
-  int *ddesc = c->d_stage, *dp = c->d_stage + desc.size(), *dt = dp + tot;
-  if (!cuda_ok(c, cudaMemcpyAsync(ddesc, desc.data(), desc.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream), "H2D desc") ||
+  int *dbad = c->d_stage, *ddesc = c->d_stage + 1, *dp = ddesc + nd, *dt = dp + tot;
+  const int lim = (int)(c->P.M / c->P.k5);         // k5 (p + T) <= M  <=>  p + T <= M / k5
+  int bad = 0;
+  if (!cuda_ok(c, cudaMemsetAsync(dbad, 0, sizeof(int), c->stream), "reset") ||
+      !cuda_ok(c, cudaMemcpyAsync(ddesc, desc, nd * sizeof(int), cudaMemcpyHostToDevice, c->stream), "H2D desc") ||
       !cuda_ok(c, cudaMemcpyAsync(dp, prompt, tot * sizeof(int), cudaMemcpyHostToDevice, c->stream), "H2D prompts") ||
       !cuda_ok(c, cudaMemcpyAsync(dt, target, tot * G * sizeof(int), cudaMemcpyHostToDevice, c->stream), "H2D targets"))
     return SF_E_CUDA;
-  sf_launch_scatter_pool(c->D, G, ddesc, n, dp, dt, c->stream);
+  sf_launch_scatter_pool(c->D, G, ddesc, n, dp, dt, lim, dbad, c->stream);
   c->launches++;
-  if (!cuda_ok(c, cudaGetLastError(), "scatter launch") || !cuda_ok(c, cudaStreamSynchronize(c->stream), "sync"))
+  if (!cuda_ok(c, cudaGetLastError(), "scatter launch") ||
+      !cuda_ok(c, cudaMemcpyAsync(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H flag") ||
+      !cuda_ok(c, cudaStreamSynchronize(c->stream), "sync"))        // the inputs are copied before return
     return SF_E_CUDA;
-  c->hn_pool = pool;
+  if (bad) {                                        // name the first invalid entry; nothing committed
+    long long off = 0;
+    for (int k = 0; k < n; ++k) {
+      for (long long a = 0; a < n_groups[k]; ++a) {
+        const long long p = prompt[off + a];
+        if (p < 0) return fail(c, SF_E_INVALID, "negative prompt length");
+        for (int m = 0; m < G; ++m) {
+          const long long T = target[(off + a) * G + m];
+          if (T < 1 || (long long)c->P.k5 * (p + T) > c->P.M) return fail(c, SF_E_INVALID, "target < 1 or k5*(p+T) > M (A27)");
+        }
+      }
+      off += n_groups[k];
+    }
+    return fail(c, SF_E_INVALID, "invalid prompt or target length");
+  }
+  sf_launch_commit_pool(c->D, ddesc, n, c->stream);
+  c->launches++;
+  if (!cuda_ok(c, cudaGetLastError(), "commit launch")) return SF_E_CUDA;
+  c->hn_pool.swap(pool);
   return SF_OK;
 }
 
@@ -380,7 +413,10 @@ sf_status sf_step(sf_ctx *c, int32_t n_windows, sf_step_stats *out) {
   DevGuard dg(c->device);
   if (n_windows < 0) return fail(c, SF_E_INVALID, "n_windows < 0");
   long long before[sf::kMetrics] = {0}, after[sf::kMetrics] = {0};
-  if (out && (st = reduce_metrics_host(c, before)) != SF_OK) return st;
+  if (out) {                                           // cumulative metrics before the call, on the device
+    sf_launch_reduce_metrics(c->D, c->n_scen, c->d_metrics + sf::kMetrics, c->stream);
+    c->launches++;
+  }
   if (c->fused && n_windows > 0) {
     prof_mark(c, 3);
     sf_launch_window_fused(c->P, c->D, c->n_scen, c->max_inst, n_windows, c->stream);
@@ -424,7 +460,15 @@ sf_status sf_step(sf_ctx *c, int32_t n_windows, sf_step_stats *out) {
   }
   if (!cuda_ok(c, cudaGetLastError(), "window launch")) return SF_E_CUDA;
   if (out) {
-    if ((st = reduce_metrics_host(c, after)) != SF_OK) return st;
+    sf_launch_reduce_metrics(c->D, c->n_scen, c->d_metrics, c->stream);
+    c->launches++;
+    long long both[2 * sf::kMetrics];
+    if (!cuda_ok(c, cudaGetLastError(), "reduce launch") ||
+        !cuda_ok(c, cudaMemcpyAsync(both, c->d_metrics, sizeof(both), cudaMemcpyDeviceToHost, c->stream), "D2H metrics") ||
+        !cuda_ok(c, cudaStreamSynchronize(c->stream), "sync"))
+      return SF_E_CUDA;
+    std::memcpy(after, both, sizeof(after));
+    std::memcpy(before, both + sf::kMetrics, sizeof(before));
     if ((st = check_errors(c, after)) != SF_OK) return st;
     out->windows = after[sf::M_WINDOWS] - before[sf::M_WINDOWS];
     out->ticks = after[sf::M_TICKS] - before[sf::M_TICKS];
