@@ -833,15 +833,32 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
     }
   }
   __syncwarp();
-  // ---------------- W2: snapshot + Eq 1 (reading R-EQ1)
+  // ---------------- W2: snapshot + Eq 1 (reading R-EQ1).  Every field of the lane's
+  // instances is loaded up front and combined with bitwise operators: short-circuit tests would
+  // turn the independent loads into a chain of memory round trips.  The same loads seed the
+  // working snapshot S, and the ledger's free counts are loaded alongside.
+  InstRegs<KS> S;
   bool ok = true;
-  for (int i = lane; i < C.I; i += 32) {
-    const long long gi = C.inst_off + i;
-    const bool quiescent = D.iintkind[gi] == INT_NONE && !D.ipullpend[gi] && D.iarr_n[gi] == 0 && D.ist[gi] != I_PULL &&
-                           D.iabort[gi] == 0;
-    const bool eq1 = D.ipv[gi] == D.iv[gi] && D.iacc[gi] == D.irun_n[gi] + D.iwn[gi] + D.ic[gi];
-    if (quiescent && !eq1) err = ERR_EQ1;
-    ok &= quiescent && eq1;
+#pragma unroll
+  for (int q = 0; q < KS; ++q) {
+    const int i = lane + 32 * q;
+    S.v[q] = 0; S.kv[q] = 0; S.n[q] = 0; S.w[q] = 0;
+    if (i < C.I) {
+      const long long gi = C.inst_off + i;
+      const int kind = D.iintkind[gi], pp = D.ipullpend[gi], an = D.iarr_n[gi], st = D.ist[gi], ab = D.iabort[gi];
+      const int pv = D.ipv[gi], v = D.iv[gi], acc = D.iacc[gi], rn = D.irun_n[gi], wn = D.iwn[gi], cc = D.ic[gi];
+      const long long kv = D.ikv[gi];
+      const bool quiescent = (kind == INT_NONE) & (pp == 0) & (an == 0) & (st != I_PULL) & (ab == 0);
+      const bool eq1 = (pv == v) & (acc == rn + wn + cc);
+      if (quiescent & !eq1) err = ERR_EQ1;
+      ok &= quiescent & eq1;
+      S.v[q] = v; S.kv[q] = kv; S.n[q] = rn; S.w[q] = wn;
+    }
+  }
+  int free_l = 0;
+  if ((int)lane <= C.eta) {
+    const int ring = (c.cu + lane) % nring;
+    free_l = P.B - D.led_nres[C.ring_off + ring] - D.led_nocc[C.ring_off + ring];
   }
   err = warp_max(err);
   if (err == ERR_EQ1) m_viol += 1;
@@ -850,24 +867,13 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
   if (valid) {
     m_valid = 1;
     // working snapshot S in registers; ledger free counts of buffers cu..cu+eta in smem
-    InstRegs<KS> S;
     int acc_delta[KS], arrn[KS];
 #pragma unroll
     for (int q = 0; q < KS; ++q) {
-      const int i = lane + 32 * q;
       acc_delta[q] = 0;
       arrn[q] = 0;
-      if (i < C.I) {
-        const long long gi = C.inst_off + i;
-        S.v[q] = D.iv[gi]; S.kv[q] = D.ikv[gi]; S.n[q] = D.irun_n[gi]; S.w[q] = D.iwn[gi];
-      } else {
-        S.v[q] = 0; S.kv[q] = 0; S.n[q] = 0; S.w[q] = 0;
-      }
     }
-    if ((int)lane <= C.eta) {
-      const int ring = (c.cu + lane) % nring;
-      sfree[lane] = P.B - D.led_nres[C.ring_off + ring] - D.led_nocc[C.ring_off + ring];
-    }
+    if ((int)lane <= C.eta) sfree[lane] = free_l;
     {
       const int bw = (P.B + 31) >> 5;
       c.use_bits = nring * bw <= kEmptyWords;
