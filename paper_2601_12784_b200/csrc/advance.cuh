@@ -654,14 +654,7 @@ __device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D,
 #ifdef SF_TIMING
   const long long t0_adv = clock64();
 #endif
-  const int s = D.inst_scen[gi];
-  const ScenConst C = D.sc[s];
-  ScenState &SS = D.ss[s];
-  if (SS.err) return;
-  const int i = gi - C.inst_off;
-  const long long t = SS.t, t_end = t + P.delta;
-  const long long lb = C.list_off + (long long)i * C.cap;
-
+  // the instance's own fields depend only on gi: issue them with the scenario lookups, not after
   InstState x;
   x.st = D.ist[gi]; x.nb = D.inb[gi]; x.until = D.iuntil[gi];
   x.pullv = D.ipullv[gi]; x.pullpend = D.ipullpend[gi];
@@ -670,6 +663,14 @@ __device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D,
   x.run_n = D.irun_n[gi]; x.whead = D.iwhead[gi]; x.wn = D.iwn[gi];
   x.arr_n = D.iarr_n[gi]; x.arr_head = 0;
   x.abortn = D.iabort[gi]; x.abortarr = D.iabort_arr[gi]; x.evn = D.iev_n[gi];
+  const int s = D.inst_scen[gi];
+  const ScenConst C = D.sc[s];
+  ScenState &SS = D.ss[s];
+  if (SS.err) return;
+  const int i = gi - C.inst_off;
+  const long long t = SS.t, t_end = t + P.delta;
+  const long long lb = C.list_off + (long long)i * C.cap;
+
   x.ticks = x.iters = x.tokens = x.comps = x.preempts = 0;
   // W6: commands to an idle instance apply at a boundary at t
   x.t_cmd = (x.st == I_IDLE && (x.pullpend || x.intkind != INT_NONE || x.abortn > 0)) ? t : kInf;
