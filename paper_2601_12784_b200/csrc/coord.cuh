@@ -184,20 +184,20 @@ static __device__ int route_group_batch(const GParams &P, const Dev &D, const Sc
   const bool cnd = (int)lane < c.I && S.v[0] >= vg;
   const long long k5l = (long long)P.k5 * l;
   {
-    long long kv = S.kv[0];
-    int n = S.n[0];
-    double Tj = Tcur;
-    bool gam = S.w[0] == 0;
-    for (int j = 0; j < nrem; ++j) {
-      double d = 0.0;
-      if (cnd && gam && kv + k5l <= P.M) {
-        const double Tn = throughput_d(P, n + 1, kv + k5l);
-        d = __dsub_rn(Tn, Tj);
-        Tj = Tn; n += 1; kv += k5l;
-      } else {
-        gam = false;
-      }
-      sg.tab[j][lane] = d;
+    // gain after j further routes here: gamma holds for the (j+1)-th route iff the lane's instance
+    // has no waiting work and kv + (j+1) k5 l <= M (kv only grows, so once false it stays false);
+    // then T(n+j+1, kv+(j+1) k5 l) - T(n+j, kv+j k5 l).  The divisions are independent of each
+    // other (branch-free div_int_rn), so they are issued together.
+    const bool ok0 = cnd && S.w[0] == 0;
+    double prev = Tcur;
+#pragma unroll
+    for (int j = 0; j < kGMax; ++j) {
+      if (j >= nrem) break;
+      const long long kvj = S.kv[0] + (long long)(j + 1) * k5l;
+      const bool gj = ok0 && kvj <= P.M;
+      const double Tn = gj ? throughput_d(P, S.n[0] + j + 1, kvj) : 0.0;
+      sg.tab[j][lane] = gj ? __dsub_rn(Tn, prev) : 0.0;
+      prev = Tn;
     }
   }
   __syncwarp();

@@ -167,7 +167,7 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
   // 32-bit products on the hot path (sf_internal.cuh tick_latency): k1, k3, kp, k5 < 2^31, M < 2^30
   if (cfg->k1_ps_per_tok < 0 || cfg->k1_ps_per_tok >= (1LL << 31) || cfg->k3_ps < 0 || cfg->k3_ps >= (1LL << 31) ||
       cfg->kprefill_ps_per_tok < 0 || cfg->kprefill_ps_per_tok >= (1LL << 31) || cfg->kv_budget_tok >= (1LL << 30) ||
-      cfg->k2_ps < 0 || cfg->k4_ps < 0)
+      cfg->k2_ps < 0 || cfg->k4_ps < 0 || cfg->k2_ps + cfg->k4_ps < 1)   // Eq 7 denominator >= 1
     return SF_E_INVALID;
   sf_ctx *c = new (std::nothrow) sf_ctx();
   if (!c) return SF_E_NOMEM;
