@@ -783,6 +783,53 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
   long long m_routes = 0, m_interrupts = 0, m_pulls = 0, m_reserves = 0, m_aborts = 0;
   const int nring = C.eta + 1;
 
+  // ---------------- one memory round trip for W0, the oldest-live scan, W2 and the ledger view:
+  // every load below depends only on C and SS, so all are issued before any of them is used.  A
+  // Consume in W0 empties one ring (patched below) and, with redundancy, may Abort members on
+  // instances (W2's fields are then reloaded).
+  int nres_r = 0, nocc_r = 0;                           // lane r <= eta: counts of ring r
+  if ((int)lane <= C.eta) { nres_r = D.led_nres[C.ring_off + lane]; nocc_r = D.led_nocc[C.ring_off + lane]; }
+  int cvb = -1;
+  {
+    const int g = c.min_live_g + (int)lane;
+    if (g < c.n_ingested) cvb = D.cvbuf[C.grp_off + g];
+  }
+  InstRegs<KS> S;
+  bool ok = true;
+  int err_eq1 = 0;
+  auto load_w2 = [&]() {
+    ok = true;
+    err_eq1 = 0;
+#pragma unroll
+    for (int q = 0; q < KS; ++q) {
+      const int i = lane + 32 * q;
+      S.v[q] = 0; S.kv[q] = 0; S.n[q] = 0; S.w[q] = 0;
+      if (i < C.I) {
+        const long long gi = C.inst_off + i;
+        const int kind = D.iintkind[gi], pp = D.ipullpend[gi], an = D.iarr_n[gi], st = D.ist[gi], ab = D.iabort[gi];
+        const int pv = D.ipv[gi], v = D.iv[gi], acc = D.iacc[gi], rn = D.irun_n[gi], wn = D.iwn[gi], cc = D.ic[gi];
+        const long long kv = D.ikv[gi];
+        // bitwise, not short-circuit: the loads stay independent
+        const bool quiescent = (kind == INT_NONE) & (pp == 0) & (an == 0) & (st != I_PULL) & (ab == 0);
+        const bool eq1 = (pv == v) & (acc == rn + wn + cc);
+        if (quiescent & !eq1) err_eq1 = ERR_EQ1;
+        ok &= quiescent & eq1;
+        S.v[q] = v; S.kv[q] = kv; S.n[q] = rn; S.w[q] = wn;
+      }
+    }
+  };
+  load_w2();
+  const int bw = (P.B + 31) >> 5;
+  c.use_bits = nring * bw <= kEmptyWords;
+  const int nw = nring * bw;
+  bool e8[8];                                           // empty-slot flags of the first 8 bitmap words
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int w = u, r = w / bw, sl = (w - r * bw) * 32 + (int)lane;
+    e8[u] = c.use_bits && w < nw && sl < P.B && D.led_st[C.led_off + (long long)r * P.B + sl] == E_EMPTY;
+  }
+  int consumed_ring = -1;
+
   // ---------------- W0: auto trainer (reading A24): publish if due, then Consume if Ready
   if (P.atw > 0) {
     int busy = SS.trainer_busy;
@@ -792,7 +839,7 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
       busy = 0;
     }
     const int ring = c.cu % nring;
-    if (!busy && D.led_nocc[C.ring_off + ring] >= P.Br) {      // Ready (App C: >= B Occupied)
+    if (!busy && __shfl_sync(0xffffffffu, nocc_r, ring) >= P.Br) {   // Ready (App C: >= B Occupied)
       CmdLog cl{c.hash, c.cmd_n, c.window, 0};
       const int retired = consume_buffer(P, D, C, SS, ring, c.cu, cl, err, nullptr);
       c.hash = cl.hash; c.cmd_n = cl.cmd_n; m_aborts = cl.aborts;
@@ -802,6 +849,8 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
         SS.batch_n += 1;
         SS.publish_at = c.t + (long long)P.atw * P.delta;
       }
+      if ((int)lane == ring) { nres_r = 0; nocc_r = 0; }
+      consumed_ring = ring;
       live -= retired;
       busy = 1;
       c.cu += 1;
@@ -811,13 +860,28 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
     if (lane == 0) SS.trainer_busy = busy;
     err = warp_max(err);
   }
+  if (consumed_ring >= 0) {
+    // the consumed ring is now all Empty; Aborted surplus members changed instance fields
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int r = u / bw, sl = (u - r * bw) * 32 + (int)lane;
+      if (r == consumed_ring) e8[u] = c.use_bits && u < nw && sl < P.B;
+    }
+    if (P.red && m_aborts > 0) load_w2();
+  }
   // oldest live group (bounds the TS bitmap scan): skip consumed groups
-  for (;;) {
-    const int g = c.min_live_g + (int)lane;
-    const bool consumed = g < c.n_ingested && D.cvbuf[C.grp_off + g] != -1;   // consumed or aborted
-    const unsigned m = __ballot_sync(0xffffffffu, !consumed);
-    if (m) { c.min_live_g += __ffs(m) - 1; break; }
-    c.min_live_g += 32;
+  {
+    bool first = consumed_ring < 0;                     // the prefetched first 32 groups are current
+    for (;;) {
+      const int g = c.min_live_g + (int)lane;
+      int cv = cvb;
+      if (!first) cv = g < c.n_ingested ? D.cvbuf[C.grp_off + g] : -1;
+      first = false;
+      const bool consumed = g < c.n_ingested && cv != -1;   // consumed or aborted
+      const unsigned m = __ballot_sync(0xffffffffu, !consumed);
+      if (m) { c.min_live_g += __ffs(m) - 1; break; }
+      c.min_live_g += 32;
+    }
   }
   // ---------------- W1: TS ingest up to (eta+1)*B live groups (A23)
   {
@@ -833,33 +897,14 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
     }
   }
   __syncwarp();
-  // ---------------- W2: snapshot + Eq 1 (reading R-EQ1).  Every field of the lane's
-  // instances is loaded up front and combined with bitwise operators: short-circuit tests would
-  // turn the independent loads into a chain of memory round trips.  The same loads seed the
-  // working snapshot S, and the ledger's free counts are loaded alongside.
-  InstRegs<KS> S;
-  bool ok = true;
-#pragma unroll
-  for (int q = 0; q < KS; ++q) {
-    const int i = lane + 32 * q;
-    S.v[q] = 0; S.kv[q] = 0; S.n[q] = 0; S.w[q] = 0;
-    if (i < C.I) {
-      const long long gi = C.inst_off + i;
-      const int kind = D.iintkind[gi], pp = D.ipullpend[gi], an = D.iarr_n[gi], st = D.ist[gi], ab = D.iabort[gi];
-      const int pv = D.ipv[gi], v = D.iv[gi], acc = D.iacc[gi], rn = D.irun_n[gi], wn = D.iwn[gi], cc = D.ic[gi];
-      const long long kv = D.ikv[gi];
-      const bool quiescent = (kind == INT_NONE) & (pp == 0) & (an == 0) & (st != I_PULL) & (ab == 0);
-      const bool eq1 = (pv == v) & (acc == rn + wn + cc);
-      if (quiescent & !eq1) err = ERR_EQ1;
-      ok &= quiescent & eq1;
-      S.v[q] = v; S.kv[q] = kv; S.n[q] = rn; S.w[q] = wn;
-    }
-  }
+  // ---------------- W2: snapshot + Eq 1 (reading R-EQ1) on the fields loaded above
   int free_l = 0;
-  if ((int)lane <= C.eta) {
+  {
     const int ring = (c.cu + lane) % nring;
-    free_l = P.B - D.led_nres[C.ring_off + ring] - D.led_nocc[C.ring_off + ring];
+    const int nr = __shfl_sync(0xffffffffu, nres_r, ring), no = __shfl_sync(0xffffffffu, nocc_r, ring);
+    if ((int)lane <= C.eta) free_l = P.B - nr - no;
   }
+  if (err_eq1) err = ERR_EQ1;
   err = warp_max(err);
   if (err == ERR_EQ1) m_viol += 1;
   const bool valid = __all_sync(0xffffffffu, ok) && !err;
@@ -874,25 +919,25 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
       arrn[q] = 0;
     }
     if ((int)lane <= C.eta) sfree[lane] = free_l;
-    {
-      const int bw = (P.B + 31) >> 5;
-      c.use_bits = nring * bw <= kEmptyWords;
-      if (c.use_bits) {
-        // 8 words per round: all slot loads of a round are issued before its ballots, so a small
-        // ledger costs one memory round trip instead of one per 32 slots
-        const int nw = nring * bw;
-        for (int w0 = 0; w0 < nw; w0 += 8) {
-          bool e[8];
+    if (c.use_bits) {
+      // ledger empty-slot bitmap: the first 8 words from the loads above, the rest (large
+      // ledgers) 8 words per round with all slot loads issued before their ballots
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int w = w0 + u, r = w / bw, sl = (w - r * bw) * 32 + (int)lane;
-            e[u] = w < nw && sl < P.B && D.led_st[C.led_off + (long long)r * P.B + sl] == E_EMPTY;
-          }
+      for (int u = 0; u < 8; ++u) {
+        const unsigned m = __ballot_sync(0xffffffffu, e8[u]);
+        if (lane == 0 && u < nw) sg.empty[u] = m;
+      }
+      for (int w0 = 8; w0 < nw; w0 += 8) {
+        bool e[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const unsigned m = __ballot_sync(0xffffffffu, e[u]);
-            if (lane == 0 && w0 + u < nw) sg.empty[w0 + u] = m;
-          }
+        for (int u = 0; u < 8; ++u) {
+          const int w = w0 + u, r = w / bw, sl = (w - r * bw) * 32 + (int)lane;
+          e[u] = w < nw && sl < P.B && D.led_st[C.led_off + (long long)r * P.B + sl] == E_EMPTY;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const unsigned m = __ballot_sync(0xffffffffu, e[u]);
+          if (lane == 0 && w0 + u < nw) sg.empty[w0 + u] = m;
         }
       }
     }
