@@ -201,7 +201,8 @@ static __device__ int route_group_batch(const GParams &P, const Dev &D, const Sc
     }
   }
   __syncwarp();
-  int jr = 0, done = 0;
+  int jr = 0, done = 0, my_sel = 0;                    // my_sel: instance of this group's lane-th route
+  const long long cmd0 = c.cmd_n;
   for (; done < nrem; ++done) {
     const double my = cnd ? sg.tab[jr][lane] : 0.0;
     // waterfall as one reduction (see route_pass): lowest version with dT >= thr, then highest dT,
@@ -240,9 +241,22 @@ static __device__ int route_group_batch(const GParams &P, const Dev &D, const Sc
           sg.arr_inst[routed] = (short)sel;
         }
       }
-      log_cmd(P, D, C, c, CMD_ROUTE, sel, id);
+      if ((int)lane == done) my_sel = sel;         // its command record: hashed after the loop
       ++routed;
     }
+  }
+  if (tentative < 0 && done > 0) {
+    // the group's Route records are consecutive commands: checksum terms lane-parallel
+    const bool mine = (int)lane < done;
+    const long long idx = cmd0 + lane;
+    const int id = id0 + 1 + (int)lane;
+    const unsigned long long h = mine ? record_hash(idx, c.window, CMD_ROUTE, my_sel, id) : 0ULL;
+    if (mine && idx < P.cmdlog_cap) {
+      long long *r = D.cmdlog + C.cmd_off + 4LL * idx;
+      r[0] = c.window; r[1] = CMD_ROUTE; r[2] = my_sel; r[3] = id;
+    }
+    c.hash += warp_sum(h);
+    c.cmd_n += done;
   }
   // the snapshot after jr routes to this lane's instance (Eq 3's S')
   for (int j = 0; j < jr; ++j) {
