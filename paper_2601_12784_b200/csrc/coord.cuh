@@ -702,11 +702,17 @@ static __device__ int interrupt_victims(const GParams &P, const Dev &D, const Sc
       atomicAdd(&D.n_interrupt[j], 1);
       atomicOr(&D.tsv_bits[C.bits_off + (id >> 5)], 1u << (id & 31));
     }
+    // one Interrupt record per victim, consecutive commands: lane k's record is the k-th
     const int nk = min(32, nvict - k0);
-    for (int a = 0; a < nk; ++a) {
-      const int ida = __shfl_sync(0xffffffffu, id, a);
-      log_cmd(P, D, C, c, CMD_INTERRUPT, i, ida);
+    const bool mine = (int)lane < nk;
+    const long long idx = c.cmd_n + lane;
+    const unsigned long long h = mine ? record_hash(idx, c.window, CMD_INTERRUPT, i, id) : 0ULL;
+    if (mine && idx < P.cmdlog_cap) {
+      long long *r = D.cmdlog + C.cmd_off + 4LL * idx;
+      r[0] = c.window; r[1] = CMD_INTERRUPT; r[2] = i; r[3] = id;
     }
+    c.hash += warp_sum(h);
+    c.cmd_n += nk;
   }
   __syncwarp();
   return nvict;
