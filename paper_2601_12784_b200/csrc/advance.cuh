@@ -413,7 +413,8 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
         //   b_j = nb + g(j-1),  g(x) = c1 x + q1 x (x+1) / 2,  q1 = k1 k5n   (Eq 7, kv growing k5 n per step)
         // and boundary j is quiet iff j <= minrem - 1, kv0 + j k5n <= M, b_j <= t_end and
         // b_j < next arrival.  m = the largest such j: g is increasing, so x = m - 1 is the floor
-        // root of g(x) = t_lim - nb, estimated in fp64 and then fixed by exact int128 checks.
+        // root of g(x) = t_lim - nb, estimated in fp64 and then fixed by exact integer checks (int64
+        // when the products provably fit, else int128).
         int mr = kDead;
 #pragma unroll
         for (int q = 0; q < kR; ++q) mr = min(mr, rem[q]);
@@ -421,33 +422,49 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
         long long m_hi = (long long)mr - 1;
         m_hi = min(m_hi, (long long)((unsigned)(P.M - x.kv) / (unsigned)k5n));   // M - kv < 2^30
         const long long t_lim = min(t_end, next_arr - 1);
-        const __int128 c1 = (__int128)P.k1i * x.kv + cn, q1 = (__int128)P.k1i * k5n;
-        auto g = [&](long long xx) -> __int128 { return c1 * xx + q1 * (((__int128)xx * (xx + 1)) >> 1); };
         long long m = 0;
+        __int128 gm = 0;                                        // g(m): b_{m+1} = nb + g(m)
 #ifdef SF_SKIP_BSEARCH
         {                                                       // A/B reference: binary search
+          const __int128 c1 = (__int128)P.k1i * x.kv + cn, q1 = (__int128)P.k1i * k5n;
+          auto g = [&](long long xx) -> __int128 { return c1 * xx + q1 * (((__int128)xx * (xx + 1)) >> 1); };
           long long lo = 0, hi = max(m_hi, 0LL);
           while (lo < hi) {
             const long long mid = (lo + hi + 1) >> 1;
             if ((__int128)x.nb + g(mid - 1) <= t_lim) lo = mid; else hi = mid - 1;
           }
           m = lo;
+          gm = g(m);
         }
 #else
         if (m_hi > 0 && x.nb <= t_lim) {
           const long long R = t_lim - x.nb;
-          const double A = 0.5 * (double)q1, Bq = (double)c1 + A, Rd = (double)R;
+          const double c1d = (double)P.k1i * (double)x.kv + (double)cn, q1d = (double)P.k1i * (double)k5n;
+          const double A = 0.5 * q1d, Bq = c1d + A, Rd = (double)R;
           const double xe = 2.0 * Rd / (Bq + sqrt(Bq * Bq + 4.0 * A * Rd));   // stable root of A x^2 + Bq x = R
           long long xx = (long long)fmin(fmax(floor(xe), 0.0), (double)(m_hi - 1));
-          while (xx + 1 <= m_hi - 1 && g(xx + 1) <= R) ++xx;
-          while (xx >= 0 && g(xx) > R) --xx;
-          m = xx + 1;
+          if (c1d < 0x1p40 && q1d < 0x1p23 && m_hi < (1LL << 19)) {
+            // every product below stays under 2^61: exact in int64
+            const long long c1 = (long long)P.k1i * x.kv + cn, q1 = (long long)P.k1i * k5n;
+            auto g = [&](long long t) -> long long { return c1 * t + q1 * ((t * (t + 1)) >> 1); };
+            while (xx + 1 <= m_hi - 1 && g(xx + 1) <= R) ++xx;
+            while (xx >= 0 && g(xx) > R) --xx;
+            m = xx + 1;
+            if (m > 0) gm = g(m);
+          } else {
+            const __int128 c1 = (__int128)P.k1i * x.kv + cn, q1 = (__int128)P.k1i * k5n;
+            auto g = [&](long long t) -> __int128 { return c1 * t + q1 * (((__int128)t * (t + 1)) >> 1); };
+            while (xx + 1 <= m_hi - 1 && g(xx + 1) <= R) ++xx;
+            while (xx >= 0 && g(xx) > R) --xx;
+            m = xx + 1;
+            if (m > 0) gm = g(m);
+          }
         }
 #endif
         if (m > 0) {
 #pragma unroll
           for (int q = 0; q < kR; ++q) rem[q] -= (int)m;
-          x.nb = (long long)((__int128)x.nb + g(m));                 // b_{m+1} = nb + g(m)
+          x.nb = (long long)((__int128)x.nb + gm);                   // b_{m+1} = nb + g(m)
           x.kv += m * k5n;
           x.tokens += m * nlive;
           x.iters += m * nlive;
