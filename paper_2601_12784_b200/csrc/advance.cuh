@@ -441,8 +441,9 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
           const long long R = t_lim - x.nb;
           const double c1d = (double)P.k1i * (double)x.kv + (double)cn, q1d = (double)P.k1i * (double)k5n;
           const double A = 0.5 * q1d, Bq = c1d + A, Rd = (double)R;
-          const double xe = 2.0 * Rd / (Bq + sqrt(Bq * Bq + 4.0 * A * Rd));   // stable root of A x^2 + Bq x = R
-          long long xx = (long long)fmin(fmax(floor(xe), 0.0), (double)(m_hi - 1));
+          // stable root of A x^2 + Bq x = R; only an estimate (the exact checks below fix it), so fp32
+          const float xe = __fdividef((float)(2.0 * Rd), (float)Bq + sqrtf((float)(Bq * Bq + 4.0 * A * Rd)));
+          long long xx = (long long)fminf(fmaxf(floorf(xe), 0.f), (float)(m_hi - 1));
           if (c1d < 0x1p40 && q1d < 0x1p23 && m_hi < (1LL << 19)) {
             // every product below stays under 2^61: exact in int64
             const long long c1 = (long long)P.k1i * x.kv + cn, q1 = (long long)P.k1i * k5n;
