@@ -728,8 +728,11 @@ static __device__ void order_arrivals_all(const GParams &P, const Dev &D, const 
     const long long te = sg.arr_t[e];
     const int inst = sg.arr_inst[e];
     int rank = 0;
-    for (int f = 0; f < n_routed; ++f)
-      rank += sg.arr_inst[f] == inst && (sg.arr_t[f] < te || (sg.arr_t[f] == te && sg.arr_id[f] < ie));
+#pragma unroll 4
+    for (int f = 0; f < n_routed; ++f) {                 // branch-free compare (no divergence)
+      const long long tf = sg.arr_t[f];
+      rank += (int)((sg.arr_inst[f] == inst) & ((tf < te) | ((tf == te) & (sg.arr_id[f] < ie))));
+    }
     const long long lb = C.list_off + (long long)inst * C.cap;
     D.arr_id[lb + rank] = ie;
     D.arr_t[lb + rank] = te;

@@ -240,7 +240,12 @@ __device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, 
       const long long te = es.t[e];
       const int ie = es.id[e];
       int rank = 0;
-      for (int f = 0; f < n; ++f) rank += es.t[f] < te || (es.t[f] == te && es.id[f] < ie);
+#pragma unroll 4
+      for (int f = 0; f < n; ++f) {                      // branch-free compare (no divergence)
+        const long long tf = es.t[f];
+        const int jf = es.id[f];
+        rank += (int)((tf < te) | ((tf == te) & (jf < ie)));
+      }
       es.srt[rank] = e;
     }
     __syncwarp();
