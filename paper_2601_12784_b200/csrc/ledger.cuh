@@ -54,8 +54,8 @@ static __device__ void delete_relocate(const GParams &P, const Dev &D, const Sce
       if (D.led_nres[C.ring_off + bb % (eta + 1)] == 0) continue;
       const long long base = ring_base(C, B, bb);
       const int hole = hb;
-      const int sl = first_slot(B, [&](int x) {
-        return D.led_st[base + x] == E_RESERVED && D.led_v[base + x] + eta >= hole;
+      const int sl = first_slot(B, [&](int x) {        // both loads issued together (bitwise &)
+        return (D.led_st[base + x] == E_RESERVED) & (D.led_v[base + x] + eta >= hole);
       });
       if (sl >= 0) { fb = bb; fs = sl; break; }
     }
@@ -121,7 +121,7 @@ static __device__ void fill_forward(const GParams &P, const Dev &D, const ScenCo
       if (D.led_nocc[C.ring_off + bb % (eta + 1)] == 0) continue;
       const long long base = ring_base(C, B, bb);
       const int hole = hb;
-      const int sl = first_slot(B, [&](int x) { return D.led_st[base + x] == E_OCCUPIED && D.led_v[base + x] <= hole; });
+      const int sl = first_slot(B, [&](int x) { return (D.led_st[base + x] == E_OCCUPIED) & (D.led_v[base + x] <= hole); });
       if (sl >= 0) { fb = bb; fs = sl; break; }
     }
     if (fb < 0) break;
