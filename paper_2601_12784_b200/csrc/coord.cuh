@@ -846,9 +846,10 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
   c.use_bits = nring * bw <= kEmptyWords;
   const int nw = nring * bw;
   bool e8[8];                                           // empty-slot flags of the first 8 bitmap words
+  const unsigned bw_inv = (65536u + bw - 1) / bw;       // u / bw == (u * bw_inv) >> 16 for u < 8, bw <= 160
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
-    const int w = u, r = w / bw, sl = (w - r * bw) * 32 + (int)lane;
+    const int w = u, r = (int)(((unsigned)w * bw_inv) >> 16), sl = (w - r * bw) * 32 + (int)lane;
     e8[u] = c.use_bits && w < nw && sl < P.B && D.led_st[C.led_off + (long long)r * P.B + sl] == E_EMPTY;
   }
   int consumed_ring = -1;
@@ -887,7 +888,7 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
     // the consumed ring is now all Empty; Aborted surplus members changed instance fields
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int r = u / bw, sl = (u - r * bw) * 32 + (int)lane;
+      const int r = (int)(((unsigned)u * bw_inv) >> 16), sl = (u - r * bw) * 32 + (int)lane;
       if (r == consumed_ring) e8[u] = c.use_bits && u < nw && sl < P.B;
     }
     if (P.red && m_aborts > 0) load_w2();
@@ -1056,10 +1057,14 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
       for (int o = 16; o > 0; o >>= 1) {
         const double oa = __shfl_xor_sync(0xffffffffu, tmax, o);
         const int oi = __shfl_xor_sync(0xffffffffu, imax, o);
-        if (oi != 0x7fffffff && (imax == 0x7fffffff || oa > tmax || (oa == tmax && oi < imax))) { tmax = oa; imax = oi; }
+        const bool bx = (oi != 0x7fffffff) & ((imax == 0x7fffffff) | (oa > tmax) | ((oa == tmax) & (oi < imax)));
+        tmax = bx ? oa : tmax;
+        imax = bx ? oi : imax;
         const double ob = __shfl_xor_sync(0xffffffffu, tmin, o);
         const int oj = __shfl_xor_sync(0xffffffffu, imin, o);
-        if (oj != 0x7fffffff && (imin == 0x7fffffff || ob < tmin || (ob == tmin && oj < imin))) { tmin = ob; imin = oj; }
+        const bool bn = (oj != 0x7fffffff) & ((imin == 0x7fffffff) | (ob < tmin) | ((ob == tmin) & (oj < imin)));
+        tmin = bn ? ob : tmin;
+        imin = bn ? oj : imin;
       }
       int case2 = -1;
       if (tmin > 0.0 && __ddiv_rn(tmax, tmin) > P.phi_tp) case2 = imax;      // A5, A6, A8
