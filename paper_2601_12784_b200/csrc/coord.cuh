@@ -201,7 +201,7 @@ static __device__ int route_group_batch(const GParams &P, const Dev &D, const Sc
     }
   }
   __syncwarp();
-  int jr = 0, done = 0, my_sel = 0;                    // my_sel: instance of this group's lane-th route
+  int jr = 0, done = 0, my_sel = 0, my_slot = 0;       // the group's lane-th route: instance, arrival slot
   const long long cmd0 = c.cmd_n;
   for (; done < nrem; ++done) {
     const double my = cnd ? sg.tab[jr][lane] : 0.0;
@@ -223,33 +223,32 @@ static __device__ int route_group_batch(const GParams &P, const Dev &D, const Sc
     if (bk != 0x7fffffff) sel = bk & 127;
     if (sel < 0) { stopped = true; break; }
     if (tentative >= 0 && sel == tentative) { hit = true; return done + 1; }
-    const int id = id0 + 1 + done;
     const int aslot = __shfl_sync(0xffffffffu, arrn, sel);
     if ((int)lane == sel) { ++jr; ++arrn; ++acc_delta; }
-    if (tentative < 0) {
-      if (lane == 0) {
-        // versionless: never interrupted, so t_ready = t (A18)
-        const long long j = C.traj_off + id;
-        D.loc[j] = L_TRANSIT;
-        D.tinst[j] = (short)sel;
-        atomicAdd(&D.n_routes[j], 1);
-        D.arr_id[C.list_off + (long long)sel * C.cap + aslot] = id;
-        D.arr_t[C.list_off + (long long)sel * C.cap + aslot] = c.t + P.r;
-        if (routed < kArrStage) {
-          sg.arr_t[routed] = c.t + P.r;
-          sg.arr_id[routed] = id;
-          sg.arr_inst[routed] = (short)sel;
-        }
-      }
-      if ((int)lane == done) my_sel = sel;         // its command record: hashed after the loop
-      ++routed;
-    }
+    if ((int)lane == done) { my_sel = sel; my_slot = aslot; }   // issued after the loop
   }
   if (tentative < 0 && done > 0) {
-    // the group's Route records are consecutive commands: checksum terms lane-parallel
+    // the group's routes, lane-parallel (nothing in the loop reads what they write); versionless
+    // members were never interrupted, so t_ready = t (A18).  Their Route records are consecutive
+    // commands: checksum terms lane-parallel too.
     const bool mine = (int)lane < done;
     const long long idx = cmd0 + lane;
     const int id = id0 + 1 + (int)lane;
+    if (mine) {
+      const long long j = C.traj_off + id;
+      D.loc[j] = L_TRANSIT;
+      D.tinst[j] = (short)my_sel;
+      atomicAdd(&D.n_routes[j], 1);
+      D.arr_id[C.list_off + (long long)my_sel * C.cap + my_slot] = id;
+      D.arr_t[C.list_off + (long long)my_sel * C.cap + my_slot] = c.t + P.r;
+      const int r = routed + (int)lane;
+      if (r < kArrStage) {
+        sg.arr_t[r] = c.t + P.r;
+        sg.arr_id[r] = id;
+        sg.arr_inst[r] = (short)my_sel;
+      }
+    }
+    routed += done;
     const unsigned long long h = mine ? record_hash(idx, c.window, CMD_ROUTE, my_sel, id) : 0ULL;
     if (mine && idx < P.cmdlog_cap) {
       long long *r = D.cmdlog + C.cmd_off + 4LL * idx;
@@ -307,7 +306,7 @@ static __device__ int route_versioned_rep(const GParams &P, const Dev &D, const 
   }
   int *const arr_id0 = D.arr_id + C.list_off;
   long long *const arr_t0 = D.arr_t + C.list_off;
-  int a = 0, my_sel = 0;                                // my_sel: the instance this lane's item went to
+  int a = 0, my_sel = 0, my_slot = 0;                   // this lane's item: instance and arrival slot
   SF_RT(0);
   for (; a < nbv; ++a) {
     // waterfall in this lane (meaningful in lane a): lowest version with dT >= thr, highest dT, lowest id
@@ -348,34 +347,32 @@ static __device__ int route_versioned_rep(const GParams &P, const Dev &D, const 
     for (int q = 0; q < kRep; ++q)
       if (q == sel) { dT[q] = ds; Tn[q] = tn; }
     SF_RT(3);
-    if (tentative < 0) {
-      // issue Route(sel, id) from the item's lane: t_arr = t_ready + r (A18); its command record
-      // is hashed / logged after the loop, lane-parallel
-      if ((int)lane == a) {
-        my_sel = sel;
-        const long long j = C.traj_off + p_id;
-        const long long t_arr = max(c.t, p_ready) + P.r;
-        D.loc[j] = L_TRANSIT;
-        D.tinst[j] = (short)sel;
-        atomicAdd(&D.n_routes[j], 1);
-        const int ao = sel * C.cap + aslot;               // < I (eta+1) B G < 2^31 (sf_create)
-        arr_id0[ao] = p_id;
-        arr_t0[ao] = t_arr;
-        if (routed < kArrStage) {
-          sg.arr_t[routed] = t_arr;
-          sg.arr_id[routed] = p_id;
-          sg.arr_inst[routed] = (short)sel;
-        }
-        atomicAnd(&D.tsv_bits[C.bits_off + (p_id >> 5)], ~(1u << (p_id & 31)));
-      }
-      SF_RT(4);
-      ++routed;
-    }
+    if ((int)lane == a) { my_sel = sel; my_slot = aslot; }
     SF_RT(5);
   }
   if (tentative < 0 && a > 0) {
-    // Route records of items 0 .. a-1 (lane = position in the command stream after cmd_n)
+    // issue Route(sel, id) for items 0 .. a-1, lane-parallel (nothing in the loop reads what these
+    // write): t_arr = t_ready + r (A18); then their command records (lane = position in the
+    // command stream after cmd_n)
     const bool mine = (int)lane < a;
+    if (mine) {
+      const long long j = C.traj_off + p_id;
+      const long long t_arr = max(c.t, p_ready) + P.r;
+      D.loc[j] = L_TRANSIT;
+      D.tinst[j] = (short)my_sel;
+      atomicAdd(&D.n_routes[j], 1);
+      const int ao = my_sel * C.cap + my_slot;            // < I (eta+1) B G < 2^31 (sf_create)
+      arr_id0[ao] = p_id;
+      arr_t0[ao] = t_arr;
+      const int r = routed + (int)lane;
+      if (r < kArrStage) {
+        sg.arr_t[r] = t_arr;
+        sg.arr_id[r] = p_id;
+        sg.arr_inst[r] = (short)my_sel;
+      }
+      atomicAnd(&D.tsv_bits[C.bits_off + (p_id >> 5)], ~(1u << (p_id & 31)));
+    }
+    routed += a;
     const long long idx = c.cmd_n + lane;
     const unsigned long long h = mine ? record_hash(idx, c.window, CMD_ROUTE, my_sel, p_id) : 0ULL;
     if (mine && idx < P.cmdlog_cap) {
