@@ -284,19 +284,21 @@ static __device__ int route_versioned_rep(const GParams &P, const Dev &D, const 
                                           bool &stop, bool &hit) {
   const unsigned lane = lane_id();
   const int I = c.I;
-  int rv[kRep];
+  int pr[kRep];                                         // waterfall priority: version, or INT_MAX if not a candidate
   double dT[kRep], Tn[kRep];
   unsigned cmask = 0;                                   // check_routable for a versioned item: v_i >= v_g
   const long long k5l = (long long)P.k5 * p_l;
+  const int k5l_i = (int)k5l;                           // <= M < 2^30 (A27); kv < 2^31 (throughput_d)
 #pragma unroll
   for (int q = 0; q < kRep; ++q) {
-    rv[q] = __shfl_sync(0xffffffffu, S.v[0], q);
+    const int rvq = __shfl_sync(0xffffffffu, S.v[0], q);
     const int nq = __shfl_sync(0xffffffffu, S.n[0], q);
     const int wq = __shfl_sync(0xffffffffu, S.w[0], q);
     const long long kvq = __shfl_sync(0xffffffffu, S.kv[0], q);
     const double Tq = __shfl_sync(0xffffffffu, Tcur, q);
-    const bool cq = q < I && rv[q] >= p_vg;
+    const bool cq = q < I && rvq >= p_vg;
     cmask |= (unsigned)cq << q;
+    pr[q] = cq ? rvq : 0x7fffffff;
     dT[q] = 0.0;
     Tn[q] = 0.0;
     if (cq && wq == 0 && kvq + k5l <= P.M) {                                           // gamma (Eq 3)
@@ -310,37 +312,36 @@ static __device__ int route_versioned_rep(const GParams &P, const Dev &D, const 
   SF_RT(0);
   for (; a < nbv; ++a) {
     // waterfall in this lane (meaningful in lane a): lowest version with dT >= thr, highest dT, lowest id
-    int bk = 0x7fffffff;
+    // (a non-candidate has pr = INT_MAX and dT = 0, so it never beats the initial bd = 0)
+    int bp = 0x7fffffff, bq = -1;
     double bd = 0.0, bt = 0.0;
 #pragma unroll
     for (int q = 0; q < kRep; ++q) {
-      const int key = (rv[q] << 7) | q;
-      const bool take = ((cmask >> q) & 1u) & (dT[q] >= p_thr) &
-                        (((key >> 7) < (bk >> 7)) | (((key >> 7) == (bk >> 7)) & (dT[q] > bd)));
-      bk = take ? key : bk;
+      const bool take = (dT[q] >= p_thr) & ((pr[q] < bp) | ((pr[q] == bp) & (dT[q] > bd)));
+      bp = take ? pr[q] : bp;
+      bq = take ? q : bq;
       bd = take ? dT[q] : bd;
       bt = take ? Tn[q] : bt;
     }
-    const int sel = __shfl_sync(0xffffffffu, bk == 0x7fffffff ? -1 : (bk & 127), a);
+    const int sel = __shfl_sync(0xffffffffu, bq, a);
     if (sel < 0) { stop = true; break; }                 // no candidate / none clears thr
     if (tentative >= 0 && sel == tentative) { hit = true; return a + 1; }
     SF_RT(1);
     // the chosen instance's snapshot entry, from its owner lane; lane a's T(n+1, kv+k5 l) there
-    const int la = __shfl_sync(0xffffffffu, p_l, a);
+    const int k5la = __shfl_sync(0xffffffffu, k5l_i, a);
     const double tb = __shfl_sync(0xffffffffu, bt, a);
     int ns = __shfl_sync(0xffffffffu, S.n[0], sel);
     int ws = __shfl_sync(0xffffffffu, S.w[0], sel);
-    long long kvs = __shfl_sync(0xffffffffu, S.kv[0], sel);
+    int kvs = __shfl_sync(0xffffffffu, (int)S.kv[0], sel);
     double Ts = __shfl_sync(0xffffffffu, Tcur, sel);
     const int aslot = __shfl_sync(0xffffffffu, arrn, sel);
-    const long long k5la = (long long)P.k5 * la;
-    const bool gamma = ws == 0 && kvs + k5la <= P.M;     // Step 5: Eq 3's S'
+    const bool gamma = ws == 0 && (long long)kvs + k5la <= P.M;   // Step 5: Eq 3's S'
     if (gamma) { ns += 1; kvs += k5la; Ts = tb; } else { ws += 1; }
     if ((int)lane == sel) { S.n[0] = ns; S.w[0] = ws; S.kv[0] = kvs; Tcur = Ts; arrn += 1; acc_delta += 1; }
     SF_RT(2);
     double ds = 0.0, tn = 0.0;
-    if (((cmask >> sel) & 1u) && ws == 0 && kvs + k5l <= P.M) {
-      tn = throughput_d(P, ns + 1, kvs + k5l);
+    if (((cmask >> sel) & 1u) && ws == 0 && (long long)kvs + k5l_i <= P.M) {
+      tn = throughput_nz(P, ns + 1, kvs + k5l_i);
       ds = __dsub_rn(tn, Ts);
     }
 #pragma unroll
