@@ -55,6 +55,7 @@ struct Cyc {                   // lane-uniform per-cycle scalars
 
 constexpr int kEmptyWords = 160;   // ledger empty-slot bitmap held in smem when (eta+1)*B <= 5120
 
+constexpr int kRepG = 4;        // route_group_batch: lane-replicated waterfall for I <= kRepG
 constexpr int kGMax = 16;       // group-batched routing for G <= kGMax (route_group_batch)
 
 struct Stage {                 // per-warp shared-memory staging
@@ -203,6 +204,37 @@ static __device__ int route_group_batch(const GParams &P, const Dev &D, const Sc
   __syncwarp();
   int jr = 0, done = 0, my_sel = 0, my_slot = 0;       // the group's lane-th route: instance, arrival slot
   const long long cmd0 = c.cmd_n;
+  if (c.I <= kRepG) {
+    // few instances: every lane evaluates the waterfall over all of them from the gain table
+    // (broadcast shared-memory reads, per-instance route counts replicated), so the decision needs
+    // no shuffle round; same order (version asc, dT desc, instance asc) as the reduction below
+    int pr[kRepG], jq[kRepG];
+#pragma unroll
+    for (int q = 0; q < kRepG; ++q) {
+      const int vq = __shfl_sync(0xffffffffu, S.v[0], q);
+      pr[q] = (q < c.I && vq >= vg) ? vq : 0x7fffffff;
+      jq[q] = 0;
+    }
+    for (; done < nrem; ++done) {
+      int bp = 0x7fffffff, sel = -1;
+      double bd = 0.0;
+#pragma unroll
+      for (int q = 0; q < kRepG; ++q) {
+        const double d = pr[q] != 0x7fffffff ? sg.tab[jq[q]][q] : 0.0;
+        const bool take = (d >= thr) & ((pr[q] < bp) | ((pr[q] == bp) & (d > bd)));
+        bp = take ? pr[q] : bp;
+        sel = take ? q : sel;
+        bd = take ? d : bd;
+      }
+      if (sel < 0) { stopped = true; break; }
+      if (tentative >= 0 && sel == tentative) { hit = true; return done + 1; }
+      const int aslot = __shfl_sync(0xffffffffu, arrn, sel);
+      if ((int)lane == sel) { ++jr; ++arrn; ++acc_delta; }
+#pragma unroll
+      for (int q = 0; q < kRepG; ++q) jq[q] += (int)(q == sel);
+      if ((int)lane == done) { my_sel = sel; my_slot = aslot; }
+    }
+  } else
   for (; done < nrem; ++done) {
     const double my = cnd ? sg.tab[jr][lane] : 0.0;
     // waterfall as one reduction (see route_pass): lowest version with dT >= thr, then highest dT,
