@@ -28,3 +28,11 @@ ph = np.diff(np.concatenate([np.zeros((len(a), 1)), a[:, 2:8]], 1), axis=1)   # 
 tot = a[:, 0]
 print("median total %.0f; median per phase [pre-sync, sync, migr, mlq2, route, arrivals]:" % np.median(tot),
       np.median(ph, 0).round(0).tolist(), "post (total - ck5):", np.median(tot - a[:, 7]))
+# share of the total coordinator cycles (all scenario-windows) spent in each phase
+sums = ph.sum(0)
+post = (tot - a[:, 7]).sum()
+allc = sums.sum() + post
+print("share of all cycles [pre-sync, sync, migr, mlq2, route, arrivals, post]:",
+      [round(float(x) / allc, 3) for x in list(sums) + [post]])
+big = a[:, 1] > 128
+print("scenario-windows with > 128 routes: %.3f, their share of cycles %.3f" % (big.mean(), tot[big].sum() / tot.sum()))
