@@ -804,10 +804,11 @@ static __device__ void order_arrivals_global(const GParams &P, const Dev &D, con
 }
 
 // One window of W0-W5 for scenario s, executed by one warp (sg: that warp's staging).
+// C = D.sc[s], passed in so that a caller can load it (it is never written by a window) before
+// waiting on the previous window's flag.
 template <int KS>
-__device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, int s, Stage &sg) {
+__device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, int s, Stage &sg, const ScenConst C) {
   const unsigned lane = lane_id();
-  const ScenConst C = D.sc[s];
   ScenState &SS = D.ss[s];
   if (SS.err) return;
 

@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(32 * kFusedWarps) k_window(GParams P, Dev D, i
   WinStage &ws = st_all[threadIdx.x >> 5];
   const int inst_off = D.sc[s].inst_off, I = D.sc[s].I;
   for (int w = 0; w < n_windows; ++w) {
-    coord_scenario<KS>(P, D, s, ws.coord);
+    coord_scenario<KS>(P, D, s, ws.coord, D.sc[s]);
     __syncwarp();
     for (int i = 0; i < I; ++i) advance_instance(P, D, inst_off + i, ws.adv);
     __syncwarp();
