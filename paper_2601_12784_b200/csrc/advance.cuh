@@ -667,7 +667,10 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
 }
 
 // One window of W6-W7 for global instance gi, executed by one warp (stage: 32*kR int2 of smem).
-__device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D, int gi, AdvStage &stage) {
+// s = D.inst_scen[gi] and C = D.sc[s] are passed in so that a caller can load them (never written
+// by a window) before waiting on the coordinator's flag.
+__device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D, int gi, AdvStage &stage, int s,
+                                                 const ScenConst C) {
   const unsigned lane = lane_id();
 #ifdef SF_TIMING
   const long long t0_adv = clock64();
@@ -681,8 +684,6 @@ __device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D,
   x.run_n = D.irun_n[gi]; x.whead = D.iwhead[gi]; x.wn = D.iwn[gi];
   x.arr_n = D.iarr_n[gi]; x.arr_head = 0;
   x.abortn = D.iabort[gi]; x.abortarr = D.iabort_arr[gi]; x.evn = D.iev_n[gi];
-  const int s = D.inst_scen[gi];
-  const ScenConst C = D.sc[s];
   ScenState &SS = D.ss[s];
   if (SS.err) return;
   const int i = gi - C.inst_off;

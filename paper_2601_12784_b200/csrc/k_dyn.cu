@@ -76,7 +76,10 @@ __global__ void __launch_bounds__(32 * kDynWarps, KS == 1 ? 16 / kDynWarps : 8 /
     if (t > 0) {                                    // advance of global instance gi
       const int gi = t - 1;
       SF_TRACE_AT(4LL * P.n_scen + 2LL * gi);
-      advance_instance(P, D, gi, ws.adv);
+      {
+        const int s = D.inst_scen[gi];
+        advance_instance(P, D, gi, ws.adv, s, D.sc[s]);
+      }
       SF_TRACE_AT(4LL * P.n_scen + 2LL * gi + 1);
       __threadfence();
       __syncwarp();
@@ -92,7 +95,7 @@ __global__ void __launch_bounds__(32 * kDynWarps, KS == 1 ? 16 / kDynWarps : 8 /
     } else {                                        // ledger of scenario s
       const int s = -t - 1;
       SF_TRACE_AT(4LL * s + 2);
-      ledger_scenario(P, D, s, ws.led);
+      ledger_scenario(P, D, s, ws.led, D.sc[s]);
       SF_TRACE_AT(4LL * s + 3);
     }
   }

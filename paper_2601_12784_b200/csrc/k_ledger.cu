@@ -9,9 +9,10 @@ __global__ void __launch_bounds__(128) k_ledger(GParams P, Dev D) {
   pdl_trigger();                                   // the next window's coordinator may be scheduled
   const int s = blockIdx.x * kLedgerWarps + (threadIdx.x >> 5);
   if (s >= P.n_scen) return;
-  if (P.pdl) warp_wait_geq(&D.f_adv[s], P.epoch * D.sc[s].I);   // all its instances advanced
+  const ScenConst C = D.sc[s];                     // constant: its load overlaps the wait
+  if (P.pdl) warp_wait_geq(&D.f_adv[s], P.epoch * C.I);   // all its instances advanced
   SF_TRACE_AT(4LL * s + 2);
-  ledger_scenario(P, D, s, stage_all[threadIdx.x >> 5]);
+  ledger_scenario(P, D, s, stage_all[threadIdx.x >> 5], C);
   SF_TRACE_AT(4LL * s + 3);
   __threadfence();                                 // this lane's writes, device-wide
   __syncwarp();

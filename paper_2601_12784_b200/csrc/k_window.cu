@@ -31,9 +31,9 @@ __global__ void __launch_bounds__(32 * kFusedWarps) k_window(GParams P, Dev D, i
   for (int w = 0; w < n_windows; ++w) {
     coord_scenario<KS>(P, D, s, ws.coord, D.sc[s]);
     __syncwarp();
-    for (int i = 0; i < I; ++i) advance_instance(P, D, inst_off + i, ws.adv);
+    for (int i = 0; i < I; ++i) advance_instance(P, D, inst_off + i, ws.adv, s, D.sc[s]);
     __syncwarp();
-    ledger_scenario(P, D, s, ws.led);
+    ledger_scenario(P, D, s, ws.led, D.sc[s]);
     __syncwarp();
   }
 }

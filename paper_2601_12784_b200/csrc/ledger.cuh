@@ -182,9 +182,9 @@ struct EvStage {
 };
 
 // One window of W8-W9 for scenario s, executed by one warp (es: that warp's staging).
-__device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, int s, EvStage &es) {
+// C = D.sc[s] (passed in, loaded by the caller before its wait).
+__device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, int s, EvStage &es, const ScenConst C) {
   const unsigned lane = lane_id();
-  const ScenConst C = D.sc[s];
   ScenState &SS = D.ss[s];
   if (SS.err) return;
   const long long t_end = SS.t + P.delta;
