@@ -810,7 +810,7 @@ template <int KS>
 __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, int s, Stage &sg, const ScenConst C) {
   const unsigned lane = lane_id();
   ScenState &SS = D.ss[s];
-  if (SS.err) return;
+  const int err0 = SS.err;    // checked after the first loads below (all reads), not before them
 
   int *sfree = sg.sfree;
 #ifdef SF_TIMING
@@ -883,6 +883,7 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
     const int w = u, r = (int)(((unsigned)w * bw_inv) >> 16), sl = (w - r * bw) * 32 + (int)lane;
     e8[u] = c.use_bits && w < nw && sl < P.B && D.led_st[C.led_off + (long long)r * P.B + sl] == E_EMPTY;
   }
+  if (err0) return;
   int consumed_ring = -1;
 
   // ---------------- W0: auto trainer (reading A24): publish if due, then Consume if Ready
