@@ -685,7 +685,7 @@ __device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D,
   x.arr_n = D.iarr_n[gi]; x.arr_head = 0;
   x.abortn = D.iabort[gi]; x.abortarr = D.iabort_arr[gi]; x.evn = D.iev_n[gi];
   ScenState &SS = D.ss[s];
-  if (SS.err) return;
+  const int err0 = SS.err;    // checked below, before the first write
   const int i = gi - C.inst_off;
   const long long t = SS.t, t_end = t + P.delta;
   const long long lb = C.list_off + (long long)i * C.cap;
@@ -694,6 +694,7 @@ __device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D,
   // W6: commands to an idle instance apply at a boundary at t
   x.t_cmd = (x.st == I_IDLE && (x.pullpend || x.intkind != INT_NONE || x.abortn > 0)) ? t : kInf;
 
+  if (err0) return;
   if (x.run_n + x.wn + x.arr_n <= 32 * kR) advance_reg(P, D, C, SS, x, lb, t_end, stage);
   else advance_global(P, D, C, SS, x, lb, t_end);
 

@@ -186,7 +186,7 @@ struct EvStage {
 __device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, int s, EvStage &es, const ScenConst C) {
   const unsigned lane = lane_id();
   ScenState &SS = D.ss[s];
-  if (SS.err) return;
+  const int err0 = SS.err;    // checked after the event-count loads below (reads + staging only)
   const long long t_end = SS.t + P.delta;
   // Pending reward events: the carry list D.ev_id[ev_off, ev_off + SS.ev_n) (not yet due in an
   // earlier window) followed by this window's completions in the instances' segments (D.iev,
@@ -202,6 +202,7 @@ __device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, 
   }
   if (lane == 0) es.ioff[C.I] = n;
   __syncwarp();
+  if (err0) return;
   auto seg_of = [&](int e) {                      // instance whose segment holds event e >= n_carry
     int lo = 0, hi = C.I - 1;
     while (lo < hi) {
