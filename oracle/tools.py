@@ -9,7 +9,7 @@ import numpy as np
 
 def fit_cost_model(kv, n_run, latency, max_rounds=50):
     kv, n_run, latency = (np.asarray(a, np.float64) for a in (kv, n_run, latency))
-    compute = n_run > np.sort(n_run)[len(n_run) // 2]          # the upper median, as in the library
+    compute = n_run > np.median(n_run)                          # initial split (reading R-FIT)
     x = None
     for _ in range(max_rounds):
         A = np.stack([kv, np.where(compute, 0.0, 1.0), np.where(compute, n_run, 0.0), np.ones_like(kv)], 1)

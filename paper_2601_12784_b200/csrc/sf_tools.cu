@@ -71,8 +71,11 @@ sf_status sf_fit_cost_model(int32_t n_samples, const double *kv, const double *n
   std::vector<int> compute(n_samples);
   std::vector<double> ns(n_run, n_run + n_samples);
   std::vector<double> sorted = ns;
-  std::nth_element(sorted.begin(), sorted.begin() + n_samples / 2, sorted.end());
-  const double med = sorted[n_samples / 2];
+  std::sort(sorted.begin(), sorted.end());
+  // the sample median (DESIGN.md §11 reading R-FIT): the middle order statistic, or the mean of
+  // the two middle ones for an even count
+  const double med = (n_samples & 1) ? sorted[n_samples / 2]
+                                     : 0.5 * (sorted[n_samples / 2 - 1] + sorted[n_samples / 2]);
   for (int i = 0; i < n_samples; ++i) compute[i] = ns[i] > med;
   double x[4] = {0, 0, 0, 0};
   for (int round = 0; round < 50; ++round) {
