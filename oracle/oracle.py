@@ -76,8 +76,12 @@ def load_oracle():
     global _lib
     if _lib is not None:
         return _lib
-    build_oracle()
-    L = C.CDLL(LIB)
+    override = os.environ.get("SFO_ORACLE_LIB")        # tests/test_oracle_mutants.py: a mutated build
+    if override:
+        L = C.CDLL(override)
+    else:
+        build_oracle()
+        L = C.CDLL(LIB)
     P, I32, I64, U32, D = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_double
     pI32, pI64 = C.POINTER(C.c_int32), C.POINTER(C.c_int64)
     sig = {
