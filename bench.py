@@ -1,24 +1,35 @@
 #!/usr/bin/env python
 """bench.py -- StaleFlow coordination step (arXiv 2601.12784) on B200.
 
-Metric (BASELINE.json): trajectory-iterations per second (one running trajectory advanced by
-one decode step of its instance) and the advance kernel's HBM roofline fraction.
+Metric (BASELINE.json): trajectory-iterations per second -- one running trajectory advanced by one
+decode step of its instance, counted identically by the oracle and the library --
+and the dominant kernel's HBM roofline fraction (algorithmic 8 B per trajectory-iteration,
+SURVEY §8(d)).
 
-Workload: the C5 configuration -- independent coordination scenarios (4 instances, B = 64,
-G = 8, eta 0..3, lognormal lengths sigma 0.25..1.5, full SF strategies) -- 4096 scenarios per
-GPU, weak scaling (rank r runs scenarios [r*4096, (r+1)*4096) of the same seeded family).  A
-"step" is one sf_step window (W0-W9 of DESIGN.md §3.1) over every scenario on the GPU, i.e.
-one pass of all of §8(a)'s rows.  L2 is flushed (512 MiB write) between timed windows.
+Workload (default C5, BASELINE.json configs[4]): independent coordination scenarios (I = 4, B = 64,
+G = 8, eta 0..3, lognormal skew 0.25..1.5, StaleFlow R/S/M).  One bench STEP is one COMPLETE run of
+the workload: every scenario of this GPU's shard from an empty state until every scenario has
+consumed its train_steps batches (C5: 1,260 windows = 10 training steps; `full_run_windows`), issued
+as sf_step calls of one trainer period (auto_train_windows windows) each.  Every §8(a) row runs in
+every window, so the timed region holds the ramp, the steady state (Consume / Publish / Alg 3 pulls
+/ Alg 4 migration) and the tail in their natural proportions.  Each step starts from a freshly
+created context (sf_create and the pool upload are outside the device-timed region; the e2e leg
+times the pool's host-to-device copy).  L2 is flushed (512 MiB write) before every step.
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+Multi-GPU: scenario s of the family belongs to rank s mod W.  --split weak (default):
+the family has 4096 x W scenarios (4096 per GPU); --split strong: one 4096-scenario family (config 5
+literally, 512 per GPU at 8 GPUs).  The only collective is the NCCL all-reduce of the int64 metric
+vector plus the max-over-ranks of the timed duration.
+
+  python bench.py [--gpus N --steps K --warmup W] [--workload C1..C5] [--split weak|strong] [--impl reference]
   torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU, NCCL)
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -32,31 +43,46 @@ METRIC = "trajectory-iterations/sec per GPU and HBM GB/s fraction at 1/2/4/8 B20
 UNIT = "trajectory-iterations/s"
 ALGO_BYTES_PER_ITER = 8          # read + write of the int32 remaining-length counter
 FALLBACK_HBM_GBS = 6650.0        # B200_PROFILING.md fallback
+KERNELS = ("k_begin_coord", "k_advance", "k_ledger", "k_window")
+NCU_FILE = os.path.join(ROOT, "profiles", "r02", "ncu_kernels.json")
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="staleflow", choices=["staleflow", "reference"])
-    ap.add_argument("--scenarios", type=int, default=4096, help="scenarios per GPU (C5 family)")
+    ap.add_argument("--workload", default="C5", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--split", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scenarios", type=int, default=4096, help="C5 scenarios per GPU (weak) / in the family (strong)")
+    ap.add_argument("--windows", type=int, default=0, help="windows per step (default: the preset's full run)")
     ap.add_argument("--flush-mb", type=int, default=512)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the steady-state / replay supplementary legs")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--profile-run", action="store_true", help="short run for ncu (no e2e / cpu legs)")
+    ap.add_argument("--profile-run", action="store_true", help="short run for ncu (timed steps only)")
     return ap.parse_args()
 
 
 def peaks():
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
-        with open(path) as f:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", d
     except Exception:
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)", {}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor() or "unknown"
 
 
 class ClockSampler:
@@ -102,72 +128,116 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def pool_arrays(p, idx, n_groups, group0=0):
+# ------------------------------------------------------------------------------ workload + shard
+def family(args, world):
+    """(preset of the whole family, this rank's scenario indices, scaling mode)."""
+    from paper_2601_12784_b200 import workload as W
+    if args.workload == "C5":
+        n = args.scenarios * world if args.split == "weak" else args.scenarios
+        full = W.preset("C5", n_scenarios=n)
+        return full, "weak" if args.split == "weak" else "strong"
+    full = W.preset(args.workload)
+    if len(full.scenarios) == 1:
+        return full, "replicas"                        # a single scenario does not shard (§8(e))
+    return full, "strong"
+
+
+def shard(full, rank, world, mode):
+    if mode == "replicas":
+        return list(range(len(full.scenarios)))
+    return [s for s in range(len(full.scenarios)) if s % world == rank]    # SURVEY §8(e): s mod W
+
+
+def pool_arrays(full, idx):
     import numpy as np
     from paper_2601_12784_b200 import workload as W
-    prs, tgs = [], []
-    for k in idx:
-        pr, tg = W.draw_lengths(p, k, n_groups, group0)
-        prs.append(pr)
-        tgs.append(tg)
+    prs, tgs = zip(*[W.draw_lengths(full, k, full.pool_groups) for k in idx])
     return np.concatenate(prs), np.concatenate(tgs)
 
 
-# ------------------------------------------------------------------------------ reference arm
+def workload_name(full, idx, mode, world):
+    return (f"{full.name} complete run: {len(idx)} scenarios on this GPU ({len(full.scenarios)} in the family, "
+            f"{mode}), {full.full_run_windows} windows = {full.train_steps} train steps each, "
+            f"sf_step calls of {full.auto_train_windows} windows")
+
+
+# ------------------------------------------------------------------------------ oracle timing
+def oracle_run(full, idx, windows, threads):
+    """The oracle, as it stands, over `windows` windows of scenarios idx: (traj_iters, seconds)."""
+    from oracle.oracle import OracleSim
+    from paper_2601_12784_b200 import workload as W
+    o = OracleSim.from_preset(full, idx)
+    for a, k in enumerate(idx):
+        pr, tg = W.draw_lengths(full, k, full.pool_groups)
+        assert o.submit(a, pr, tg) == 0
+    t0 = time.perf_counter()
+    assert o.step(windows, threads) == 0
+    dt = time.perf_counter() - t0
+    return int(o.metrics()[2]), dt
+
+
+def oracle_sample(full, idx, target_s):
+    """A bounded sample of the workload sized to ~target_s of host time: the first n scenarios of the
+    shard over the full run (multi-scenario configs, all host threads), or one scenario over the
+    first w windows (single-scenario configs, one thread: the oracle is sequential per scenario)."""
+    cores = os.cpu_count() or 1
+    W_full = full.full_run_windows
+    if len(idx) == 1:
+        w = min(W_full, 200)
+        while True:
+            it, dt = oracle_run(full, idx, w, 1)
+            if dt >= 0.3 * target_s or w >= W_full:
+                return {"n": 1, "windows": w, "threads": 1, "iters": it, "s": dt}
+            w = min(W_full, max(w + 1, int(w * target_s / max(dt, 1e-3))))
+    n = min(len(idx), max(1, cores))
+    while True:
+        it, dt = oracle_run(full, idx[:n], W_full, cores)
+        if dt >= 0.3 * target_s or n >= len(idx):
+            return {"n": n, "windows": W_full, "threads": cores, "iters": it, "s": dt}
+        n = min(len(idx), max(n + 1, int(n * target_s / max(dt, 1e-3))))
+
+
+def cpu_baseline_of(full, idx, smp, kind="oracle"):
+    return {"value": smp["iters"] / smp["s"], "unit": UNIT, "cores": smp["threads"], "kind": kind,
+            "cpu_model": cpu_model(), "host_cpus": os.cpu_count(),
+            "sample": f"{smp['n']} of {len(idx)} {full.name} scenarios x windows 0..{smp['windows'] - 1} "
+                      f"(the complete run is {full.full_run_windows}), {smp['s']:.1f} s on {smp['threads']} threads"}
+
+
 def run_reference(args, rank, world):
-    """The oracle, as it stands, on the host cores: same metric/config, bounded sample."""
+    """--impl reference: the oracle as it stands on the host cores, same workload / metric; each step
+    a bounded sample of the workload (rank 0 only under torchrun)."""
     if rank != 0:
         return
-    from paper_2601_12784_b200 import workload as W
-    full = W.preset("C5", n_scenarios=args.scenarios)
-    cpu = oracle_rate(full, list(range(args.scenarios)), args.warmup, args.steps, args.cpu_seconds)
-    v = cpu["value"]
+    full, mode = family(args, world)
+    idx = shard(full, 0, world, mode)
+    per_step = max(1.0, args.cpu_seconds / max(1, args.steps + args.warmup))
+    smp = oracle_sample(full, idx, per_step)
+    sub = idx[:smp["n"]]
+    for _ in range(args.warmup):
+        oracle_run(full, sub, smp["windows"], smp["threads"])
+    its, secs = 0, 0.0
+    for _ in range(args.steps):
+        it, dt = oracle_run(full, sub, smp["windows"], smp["threads"])
+        its += it
+        secs += dt
+    v = its / secs
+    smp_t = dict(smp, iters=its, s=secs)
+    cpu = cpu_baseline_of(full, idx, smp_t)
+    cpu["sample"] += f" per step, {args.steps} steps"
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-           "config": {"workload": f"C5 ({cpu['sample']})", "windows_per_step": 1},
+           "warmup": args.warmup, "ms_per_step": secs * 1e3 / args.steps, "higher_is_better": True,
+           "scaling": "weak" if mode != "strong" else "strong", "vs_baseline": None, "dtype": "int32",
+           "data": "synthetic", "config": {"workload": workload_name(full, idx, mode, world) + " (oracle sample)",
+                                            "windows_per_step": smp["windows"]},
            "cpu_baseline": cpu,
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
-# ------------------------------------------------------------------------------ cpu baseline
-def oracle_rate(full, idx, warmup, steps, target_s, n_first=64):
-    """The oracle (as it stands) on host cores over the SAME window range as the timed GPU
-    region (warm-up windows untimed), on a bounded sample of scenarios sized to ~target_s."""
-    from oracle.oracle import OracleSim
-    from paper_2601_12784_b200 import workload as W
-    cores = os.cpu_count() or 1
-    n = min(n_first, len(idx))
-    while True:
-        sample = idx[:n]
-        o = OracleSim.from_preset(full, sample)
-        for a, k in enumerate(sample):
-            pr, tg = W.draw_lengths(full, k, full.pool_groups)
-            assert o.submit(a, pr, tg) == 0
-        o.step(warmup, cores)
-        m0 = o.metrics()
-        t0 = time.perf_counter()
-        for _ in range(steps):
-            o.step(1, cores)
-        dt = time.perf_counter() - t0
-        it = int(o.metrics()[2] - m0[2])
-        if dt >= 0.3 * target_s or n >= len(idx):
-            break
-        n = min(len(idx), max(n + 1, int(n * target_s / max(dt, 1e-3))))
-    return {"value": it / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{n} of {len(idx)} C5 scenarios, windows {warmup}..{warmup + steps - 1} "
-                      f"(same range as the timed GPU steps), {dt:.1f} s on {cores} threads"}
-
-
-def shard(n_per_rank: int, rank: int):
-    """Weak scaling: rank r owns scenarios [r*S, (r+1)*S) of one seeded C5 family."""
-    return list(range(rank * n_per_rank, (rank + 1) * n_per_rank))
-
-
+# ------------------------------------------------------------------------------ GPU arm
 def reduce_metrics(vec, world, dist):
     """All-reduce of the int64 metrics vector: sums, except slot 30 (max time)."""
-    import torch
     if world > 1:
         mx = vec[30].clone()
         dist.all_reduce(vec, op=dist.ReduceOp.SUM)
@@ -176,7 +246,6 @@ def reduce_metrics(vec, world, dist):
     return vec
 
 
-# ------------------------------------------------------------------------------ main arm
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -195,13 +264,17 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
-    S = args.scenarios
-    full = W.preset("C5", n_scenarios=S * world)
-    idx = shard(S, rank)
+    full, mode = family(args, world)
+    idx = shard(full, rank, world, mode)
+    S = len(idx)
     p = W.preset_scenario_slice(full, idx)
-    ctx = StaleFlow.from_preset(p, stream=stream)
-    pr, tg = pool_arrays(full, idx, full.pool_groups)
-    assert ctx.submit_many(np.arange(S), np.full(S, full.pool_groups), pr, tg) == 0
+    windows = args.windows or full.full_run_windows
+    per_call = full.auto_train_windows
+    pr, tg = pool_arrays(full, idx)
+    hp = [torch.from_numpy(np.arange(S, dtype=np.int32)).pin_memory(),
+          torch.from_numpy(np.full(S, full.pool_groups, np.int32)).pin_memory(),
+          torch.from_numpy(pr).pin_memory(), torch.from_numpy(tg).pin_memory()]
+    h2d_bytes = sum(x.numel() * x.element_size() for x in hp)
     flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device="cuda")
 
     def barrier():
@@ -209,201 +282,170 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    ctx.step(args.warmup)
+    def fresh(submit=True):
+        ctx = StaleFlow.from_preset(p, stream=stream)
+        if submit:
+            assert ctx.submit_many_ptr(S, *(x.data_ptr() for x in hp)) == 0
+        return ctx
+
+    def run_windows(ctx, n):
+        for w0 in range(0, n, per_call):
+            ctx.step(min(per_call, n - w0))
+
+    # ---------------- warm-up: W complete runs (untimed)
+    for _ in range(args.warmup):
+        ctx = fresh()
+        run_windows(ctx, windows)
+        ctx.close()
     barrier()
-    m0 = ctx.metrics()
-    l0 = ctx.kernel_launches
+
+    # ---------------- timed: K complete runs, device time on the context stream
     clocks = ClockSampler(local)
     clocks.start()
-    evs = []
-    barrier()
+    ms, launches = 0.0, 0
+    dm = np.zeros(32, np.int64)
     for _ in range(args.steps):
+        ctx = fresh()
         flush.zero_()                                   # L2 flush, outside the timed events
+        barrier()
+        m0 = ctx.metrics()
+        l0 = ctx.kernel_launches
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(stream)
-        ctx.step(1)
+        run_windows(ctx, windows)
         e.record(stream)
-        evs.append((s, e))
-    barrier()
-    ms = sum(s.elapsed_time(e) for s, e in evs)
+        barrier()
+        ms += s.elapsed_time(e)
+        launches += ctx.kernel_launches - l0
+        m1 = ctx.metrics()
+        dm += (m1 - m0).astype(np.int64)
+        ctx.close()
     clk = clocks.stop()
-    m1 = ctx.metrics()
-    launches = ctx.kernel_launches - l0 - 1             # minus the metrics reduction at m1
-    local_iters = int(m1[2] - m0[2])
+    dmt = torch.tensor(dm, device="cuda")
+    tm = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    reduce_metrics(dmt, world, dist)                    # the metrics all-reduce (NCCL over NVLink)
+    if world > 1:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    total_iters = int(dmt[2].item())
+    max_ms = float(tm.item())
+    value = total_iters / (max_ms / 1e3)
+    assert int(dmt[12].item()) == 0 and int(dmt[29].item()) == 0, "protocol violation / poisoned scenario"
 
-    # per-kernel durations: the timed windows overlap their three kernels (programmatic dependent
-    # launch), so CUDA events between the kernels would serialize them.  The simulation is
-    # deterministic, so a second context replays exactly the same windows (same inputs, same work)
-    # with events recorded around every launch; those give the dominant kernel and its duration.
-    rctx = StaleFlow.from_preset(p, stream=stream)
-    assert rctx.submit_many(np.arange(S), np.full(S, full.pool_groups), pr, tg) == 0
-    rctx.step(args.warmup)
+    # ---------------- roofline of the dominant kernel: one more complete run with CUDA events around
+    # every launch (the library records them on the context stream, launches serialized); the
+    # simulation is deterministic, so it is the same work as each timed step
+    hbm, peak_src, _ = peaks()
+    rctx = fresh()
+    flush.zero_()
     barrier()
     rctx.profile(True)
-    for _ in range(args.steps):
-        flush.zero_()
-        rctx.step(1)
+    run_windows(rctx, windows)
     barrier()
     rctx.profile(False)
     kern_ms, kern_n = rctx.profile_read()
-    replay_ok = bool((rctx.metrics() == m1).all())      # identical simulation (work and results)
+    replay_iters = int(rctx.metrics()[2])
     rctx.close()
-    dm = torch.tensor((m1 - m0).astype(np.int64), device="cuda")
-    tm = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    reduce_metrics(dm, world, dist)                     # the metrics all-reduce (NCCL over NVLink)
-    if world > 1:
-        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-    total_iters = int(dm[2].item())
-    max_ms = float(tm.item())
-    value = total_iters / (max_ms / 1e3)
-
-    # ---------------- roofline of the dominant kernel from the replay's CUDA events
-    hbm, peak_src, _ = peaks()
-    kid = int(np.argmax(kern_ms))                       # dominant kernel of the step
-    kname = ("k_begin_coord", "k_advance", "k_ledger", "k_window")[kid]
-    adv_ms_per_launch = kern_ms[kid] / max(1, kern_n[kid])
-    bytes_per_launch = ALGO_BYTES_PER_ITER * local_iters / max(1, kern_n[kid])
-    achieved = bytes_per_launch / (adv_ms_per_launch / 1e3) / 1e9
-    traffic = None                                      # ncu dram bytes per launch of that kernel
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
+    kid = int(np.argmax(kern_ms))
+    kname = KERNELS[kid]
+    ms_per_launch = kern_ms[kid] / max(1, kern_n[kid])
+    bytes_per_launch = ALGO_BYTES_PER_ITER * replay_iters / max(1, kern_n[kid])
+    achieved = bytes_per_launch / (ms_per_launch / 1e3) / 1e9
+    ncu = {}
+    if os.path.exists(NCU_FILE):
         try:
-            for k, v in json.load(open(tpath))["dram_bytes_per_launch"].items():
-                if kname in k:
-                    traffic = v
+            ncu = json.load(open(NCU_FILE))
         except Exception:
-            traffic = None
-    share = {k: kern_ms[i] / max(1e-9, kern_ms.sum())
-             for i, k in enumerate(("coordinate", "advance", "ledger", "fused_window")) if kern_n[i]}
+            ncu = {}
+    kn = ncu.get("kernels", {})
+    traffic = kn.get(kname, {}).get("dram_bytes_per_launch")
+    share = {KERNELS[i]: float(kern_ms[i] / max(1e-9, kern_ms.sum())) for i in range(4) if kern_n[i]}
+    issue = {k: {"issue_active_frac": v.get("issue_active_frac"), "warps_per_sched": v.get("eligible_warps_per_sched"),
+                 "achieved_occupancy": v.get("achieved_occupancy")} for k, v in kn.items()} or None
 
-    # ---------------- e2e: the same metric through the C ABI with host buffers
+    # ---------------- e2e: the same complete runs through the C ABI with host buffers: per step the
+    # pool's H2D from pinned memory (sf_submit_prompts_many), every window, the metrics' D2H
     e2e = None
     if not args.no_e2e and not args.profile_run:
-        e2e = run_e2e(args, full, idx, stream, world, barrier)
-
-    # ---------------- supplementary: the same K windows as ONE sf_step call (with programmatic
-    # dependent launch a scenario starts its next window as soon as its own previous one is done,
-    # so windows pipeline across scenarios; L2 not flushed between windows because there is no
-    # host boundary).  Not the headline.
-    multi = None
-    if not args.profile_run and not args.no_e2e:
-        ctx2 = StaleFlow.from_preset(p, stream=stream)
-        assert ctx2.submit_many(np.arange(S), np.full(S, full.pool_groups), pr, tg) == 0
-        ctx2.step(args.warmup)
-        barrier()
-        n0 = ctx2.metrics()[2]
-        s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s2.record(stream)
-        ctx2.step(args.steps)
-        e2.record(stream)
-        barrier()
-        it2 = torch.tensor([int(ctx2.metrics()[2] - n0)], dtype=torch.int64, device="cuda")
-        ms2 = torch.tensor([s2.elapsed_time(e2)], dtype=torch.float64, device="cuda")
+        its, secs = 0, 0.0
+        for k in range(max(1, args.steps)):
+            ctx = fresh(submit=False)
+            barrier()
+            t0 = time.perf_counter()
+            assert ctx.submit_many_ptr(S, *(x.data_ptr() for x in hp)) == 0
+            run_windows(ctx, windows)
+            m = ctx.metrics()                            # syncs the stream; D2H of the result
+            secs += time.perf_counter() - t0
+            its += int(m[2])
+            ctx.close()
+        it_t = torch.tensor([its], dtype=torch.int64, device="cuda")
+        se_t = torch.tensor([secs], dtype=torch.float64, device="cuda")
         if world > 1:
-            dist.all_reduce(it2, op=dist.ReduceOp.SUM)
-            dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
-        multi = {"value": int(it2.item()) / (float(ms2.item()) / 1e3), "unit": UNIT,
-                 "windows_per_call": args.steps, "launch": "3 kernels per window with programmatic dependent launch, one sf_step call",
-                 "ms_per_window": float(ms2.item()) / args.steps}
-        ctx2.close()
+            dist.all_reduce(it_t, op=dist.ReduceOp.SUM)
+            dist.all_reduce(se_t, op=dist.ReduceOp.MAX)
+        e2e = {"value": int(it_t.item()) / float(se_t.item()), "unit": UNIT, "h2d_bytes_per_step": h2d_bytes,
+               "d2h_bytes_per_step": 32 * 8,
+               "note": "per step: pinned H2D of the whole prompt pool (sf_submit_prompts_many), every window "
+                       "(sf_step per trainer period), D2H of the metric vector; host wall clock, max over ranks"}
+
+    # ---------------- supplementary: steady state only (windows 150..449), as sf_step calls of one
+    # window with L2 flushed before each (round 1's definition) and of one trainer period
+    steady = None
+    if not args.no_extra and not args.profile_run and full.name == "C5" and windows >= 450:
+        steady = {}
+        for label, pc in (("per_window_calls", 1), ("per_trainer_period_calls", per_call)):
+            ctx = fresh()
+            run_windows(ctx, 150)
+            barrier()
+            n0 = ctx.metrics()[2]
+            t = 0.0
+            for w0 in range(150, 450, pc):
+                flush.zero_()
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record(stream)
+                ctx.step(pc)
+                e.record(stream)
+                e.synchronize()
+                t += s.elapsed_time(e)
+            it = int(ctx.metrics()[2] - n0)
+            ctx.close()
+            steady[label] = {"value": it / (t / 1e3), "ms_per_window": t / 300}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile_run:
-        cpu = oracle_rate(full, idx, args.warmup, args.steps, args.cpu_seconds)
+        cpu = cpu_baseline_of(full, idx, oracle_sample(full, idx, args.cpu_seconds))
 
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": "C5: independent coordination scenarios (I=4, B=64, G=8, eta 0..3, "
-                                   "lognormal skew 0.25..1.5, SF R/S/M), 1 step = 1 window over all",
-                       "scenarios_per_gpu": S, "global_scenarios": S * world, "windows_per_step": 1,
-                       "parallelism": f"scenario-sharded x{world}", "l2": f"flushed ({args.flush_mb} MiB write) "
-                                                                          "between timed windows"},
-            "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm,
-                         "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+            "scaling": "strong" if mode == "strong" else "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic",
+            "config": {"workload": workload_name(full, idx, mode, world), "windows_per_step": windows,
+                       "windows_per_call": per_call, "scenarios_per_gpu": S, "global_scenarios": len(full.scenarios),
+                       "split": mode, "parallelism": f"scenario-sharded x{world} (s mod W)" if mode != "replicas"
+                       else f"replicas x{world}",
+                       "l2": f"flushed ({args.flush_mb} MiB write) before every step"},
+            "per_gpu": value / world,
+            "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm, "peak_source": peak_src,
+                         "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                          "algorithmic_bytes_per_traj_iter": ALGO_BYTES_PER_ITER,
-                         "launches": int(kern_n[kid]), "ms_per_launch": adv_ms_per_launch,
-                         "step_share": share,
-                         "timing": "CUDA events around each launch in a serialized replay of the timed windows "
-                                   "(same inputs and work; the timed run overlaps kernels via PDL)",
-                         "replay_identical": replay_ok},
+                         "launches": int(kern_n[kid]), "ms_per_launch": ms_per_launch, "step_share": share,
+                         "timing": "CUDA events around every launch in a serialized replay of one step "
+                                   "(same inputs and work; the timed steps overlap kernels via PDL)",
+                         "issue_slots_ncu": issue, "ncu_source": os.path.relpath(NCU_FILE, ROOT) if ncu else None},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "multi_window": multi,
+            "steady_state": steady,
             "gpu_launches": int(launches),
             "clocks": clk,
-            "sim": {"routes": int(dm[5].item()), "completions": int(dm[4].item()), "batches": int(dm[9].item()),
-                    "interrupts": int(dm[6].item()), "pulls": int(dm[7].item()),
-                    "invalid_snapshots": int(dm[11].item()), "violations": int(dm[12].item())},
+            "sim": {"routes": int(dmt[5].item()), "completions": int(dmt[4].item()), "batches": int(dmt[9].item()),
+                    "interrupts": int(dmt[6].item()), "pulls": int(dmt[7].item()),
+                    "invalid_snapshots": int(dmt[11].item()), "violations": int(dmt[12].item()),
+                    "staleness_hist": [int(x) for x in dmt[16:25].tolist()]},
         }
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
-
-
-def run_e2e(args, full, idx, stream, world, barrier):
-    """Per step: H2D of that window's new prompts from pinned host memory through
-    sf_submit_prompts_many, sf_step (one window), D2H of the step's metric deltas."""
-    import numpy as np
-    import torch
-    import torch.distributed as dist
-    from paper_2601_12784_b200 import workload as W
-    from paper_2601_12784_b200.staleflow import StaleFlow
-    S = len(idx)
-    p = W.preset_scenario_slice(full, idx)
-    ctx = StaleFlow.from_preset(p, stream=stream)
-    B = full.batch_size
-    eta_max = max(s.eta for s in p.scenarios)
-    first = (eta_max + 1) * B                              # the initial TS fill
-    per_step = B // 8                                      # 8 groups/scenario/window keeps the TS fed
-    total_windows = args.warmup + args.steps
-    pool = full.pool_groups
-    ctx_first = pool_arrays(full, idx, first)
-    assert ctx.submit_many(np.arange(S), np.full(S, first), *ctx_first) == 0
-    submitted = first
-    chunks = []
-    for w in range(total_windows):
-        ng = min(per_step, pool - submitted)
-        if ng <= 0:
-            chunks.append(None)
-            continue
-        pr, tg = pool_arrays(full, idx, ng, submitted)
-        hp = [torch.from_numpy(np.arange(S, dtype=np.int32)).pin_memory(),
-              torch.from_numpy(np.full(S, ng, np.int32)).pin_memory(),
-              torch.from_numpy(pr).pin_memory(), torch.from_numpy(tg).pin_memory()]
-        chunks.append((ng, hp))
-        submitted += ng
-    iters = 0
-    h2d = d2h = 0
-    t_total = 0.0
-    for w in range(total_windows):
-        timed = w >= args.warmup
-        if timed and w == args.warmup:
-            barrier()
-        t0 = time.perf_counter()
-        if chunks[w] is not None:
-            ng, hp = chunks[w]
-            assert ctx.submit_many_ptr(S, *(x.data_ptr() for x in hp)) == 0
-            if timed:
-                h2d += sum(x.numel() * 4 for x in hp)
-        st = ctx.step(1, stats=True)                       # syncs + D2H of the metric deltas
-        t1 = time.perf_counter()
-        if timed:
-            t_total += t1 - t0
-            iters += st["traj_iters"]
-            d2h += 2 * 32 * 8
-    tt = torch.tensor([t_total], dtype=torch.float64, device="cuda")
-    it = torch.tensor([iters], dtype=torch.int64, device="cuda")
-    if world > 1:
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        dist.all_reduce(it, op=dist.ReduceOp.SUM)
-    ctx.close()
-    return {"value": int(it.item()) / float(tt.item()), "unit": UNIT,
-            "h2d_bytes_per_step": h2d // max(1, args.steps), "d2h_bytes_per_step": d2h // max(1, args.steps),
-            "note": "per window: pinned H2D of new prompts (sf_submit_prompts_many), sf_step, D2H of metrics; "
-                    "host wall clock, max over ranks"}
 
 
 if __name__ == "__main__":

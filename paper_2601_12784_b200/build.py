@@ -31,15 +31,18 @@ def needs_build() -> bool:
     return os.path.getmtime(LIB) < max(os.path.getmtime(d) for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, extra=()) -> str:
+    """Compile every csrc/*.cu for sm_100a and link `out`.  `extra` nvcc flags (e.g. -DSF_TIMING)
+    build an instrumented variant next to the product library (tools/timing_profile.py)."""
+    if out == LIB and not extra and not force and not needs_build():
         return LIB
     objs = []
-    os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
+    bdir = os.path.join(HERE, "build" if out == LIB else "build_" + os.path.basename(out).replace(".", "_"))
+    os.makedirs(bdir, exist_ok=True)
     procs = []
     for src in sources():
-        obj = os.path.join(HERE, "build", os.path.basename(src)[:-3] + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        obj = os.path.join(bdir, os.path.basename(src)[:-3] + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((subprocess.Popen(cmd), cmd))
@@ -47,11 +50,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for p, cmd in procs:
         if p.wait() != 0:
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = out + f".tmp{os.getpid()}"
     subprocess.run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs], check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python -m paper_2601_12784_b200.build [--force] [-v] [--out lib.so -DFLAG ...]
+    argv = sys.argv[1:]
+    out = LIB
+    if "--out" in argv:
+        out = os.path.abspath(argv[argv.index("--out") + 1])
+    extra = [a for a in argv if a.startswith("-D")]
+    print(build(force="--force" in argv, verbose="-v" in argv, out=out, extra=extra))

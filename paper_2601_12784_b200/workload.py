@@ -12,7 +12,9 @@ from zero and clamped to [1, cap]. Group correlation: a shared per-group
 normal z_g plus a per-member z_m, so "trajectories within a group tend to be
 either all long or all short".
 
-Presets C1..C5 follow SURVEY §8(d) / BASELINE.json `configs`. Time constants
+Presets C1..C5 follow SURVEY §8(d) / BASELINE.json `configs`.  `full_run_windows` is the window
+count by which every scenario of the preset has reached its train-step count (measured once on the
+oracle; tests/test_gpu_fulllength.py asserts it), i.e. the length of one complete run. Time constants
 are integer picoseconds (reading A1): Table 6 gives
 k1 = 7.28e-8 s/token = 72,800 ps, k2 = 1.72e-3 s, k3 = 1.25e-4 s,
 k4 = 1.07e-2 s.
@@ -126,6 +128,7 @@ class Preset:
     extra_groups: int = 0                 # batch-level redundant rollout (App C)
     extra_members: int = 0                # group-level redundant rollout (P:473 footnote)
     filter_prob: float = 0.0              # P(group carries no learning signal), filtered (P:413 (2))
+    full_run_windows: int = 0             # windows until every scenario has train_steps batches
 
     @property
     def members(self) -> int:
@@ -189,17 +192,17 @@ def preset(name: str, n_scenarios: Optional[int] = None) -> Preset:
     if name == "C1":
         return Preset("C1", [Scenario(1, 4, STRAT_SF, 1)], 64, 8,
                       LengthDist("uniform", 64, 512), LengthDist("uniform", 128, 2048),
-                      131_072, 15, 10)
+                      131_072, 15, 10, full_run_windows=600)
     if name == "C2":
         return Preset("C2", [Scenario(2, 16, STRAT_R, 2)], 512, 16,
                       LengthDist("uniform", 64, 1024),
                       LengthDist("lognormal", median=2048, sigma_g=0.8, sigma_m=0.6, cap=16_384),
-                      1_048_576, 200, 10)
+                      1_048_576, 200, 10, full_run_windows=10_500)
     if name == "C3":
         return Preset("C3", [Scenario(3, 32, STRAT_R | STRAT_M, 3)], 128, 16,
                       LengthDist("uniform", 64, 2048),
                       LengthDist("lognormal", median=4096, sigma_g=0.8, sigma_m=0.6, cap=32_768),
-                      1_048_576, 60, 10)
+                      1_048_576, 60, 10, full_run_windows=4_200)
     if name == "C4":
         sc = []
         for eta in range(5):
@@ -211,7 +214,7 @@ def preset(name: str, n_scenarios: Optional[int] = None) -> Preset:
             sc = sc[:n_scenarios]
         return Preset("C4", sc, 1024, 16, LengthDist("uniform", 64, 1024),
                       LengthDist("lognormal", median=2048, sigma_g=0.8, sigma_m=0.6, cap=16_384),
-                      1_048_576, 120, 5)
+                      1_048_576, 120, 5, full_run_windows=22_600)
     if name == "C5":
         n = 4096 if n_scenarios is None else n_scenarios
         sc = []
@@ -222,7 +225,7 @@ def preset(name: str, n_scenarios: Optional[int] = None) -> Preset:
             sc.append(Scenario(eta, 4, STRAT_SF, 5000 + seed, skews[skew_i]))
         return Preset("C5", sc, 64, 8, LengthDist("uniform", 64, 512),
                       LengthDist("lognormal", median=768, cap=4096),
-                      131_072, 15, 10)
+                      131_072, 15, 10, full_run_windows=1_260)
     if name == "C5R":
         # C5 with App C's redundancy ratios (+1/16 of the batch, +1/16 of the group,
         # rounded up to whole groups / members): 64 + 4 groups, 8 + 1 members; 1/16 of the groups
