@@ -74,6 +74,12 @@ typedef struct {
                                       /*   members are rolled out per group; a group completes   */
                                       /*   at group_size rewarded members and its other members  */
                                       /*   are Aborted at once (P:473 footnote)      */
+  int32_t watchdog_windows;           /* > 0, auto trainer only: a scenario that makes no progress */
+                                      /*   for this many consecutive windows with nothing pending */
+                                      /*   (instances idle, no reward in flight, trainer idle)    */
+                                      /*   while groups remain unconsumed is deadlocked (SPEC     */
+                                      /*   S:494): it is poisoned and sf_step returns SF_E_STATE. */
+                                      /*   0 = off (a streaming caller may still submit prompts)  */
   int32_t device;                     /* CUDA device ordinal                                     */
   void *cuda_stream;                  /* cudaStream_t (e.g. torch.cuda.Stream().cuda_stream)     */
 } sf_config;

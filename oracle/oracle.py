@@ -54,7 +54,7 @@ class Config(C.Structure):
         ("mu", C.c_double), ("phi_tp", C.c_double), ("phi_wait", C.c_int32),
         ("delta", C.c_int64), ("r", C.c_int64), ("q", C.c_int64), ("R", C.c_int64),
         ("strategy", C.c_uint32), ("atw", C.c_int32), ("pool_capacity_groups", C.c_int32),
-        ("extra_groups", C.c_int32), ("extra_members", C.c_int32),
+        ("extra_groups", C.c_int32), ("extra_members", C.c_int32), ("watchdog_windows", C.c_int32),
     ]
 
 

@@ -13,6 +13,7 @@
 #include "sf_oracle.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <deque>
 #include <limits>
@@ -372,8 +373,10 @@ struct Scen {
   int I = 0, eta = 0, B = 0, G = 0; uint32_t strategy = 0;
   int Br = 0, Gr = 0;              // batch size and required members; B, G include redundancy (App C)
   int64_t delta = 0, r = 0, q = 0, R = 0; int atw = 0; int pool_cap = 0;
+  int wd = 0, wd_idle = 0; int64_t wd_sig = 0;     // deadlock watchdog
   std::vector<Traj> traj; std::vector<Group> grp;
   int n_pool = 0, n_ingested = 0, live = 0;
+  int settled = 0;                 // groups [0, settled) have every member DONE / CONSUMED / ABORTED
   std::vector<Inst> inst;
   sfo_ledger L;
   int ps = 0; int64_t t = 0, window = 0;
@@ -476,14 +479,24 @@ void consume(Scen &s, int *vbuf, int *gids, int *gv) {
 void coordinate(Scen &s) {
   const Params &P = s.P;
   const int64_t t = s.t;
+  // Those three states are final (a trajectory never leaves them for the TS), so the TS scans below
+  // can start after the leading run of groups whose members are all in them (a scan bound only).
+  auto final_state = [&](int j) { return s.traj[j].st == L_DONE || s.traj[j].st == L_CONSUMED || s.traj[j].st == L_ABORTED; };
+  while (s.settled < s.n_ingested) {
+    bool all = true;
+    for (int m = 0; m < s.G; ++m) all = all && final_state(s.settled * s.G + m);
+    if (!all) break;
+    s.settled++;
+  }
+  const int j0 = s.settled * s.G;
   // get_ts_trajs(): trajectories resident in the TS, MLQ-ordered.
   auto ts_items = [&]() {
     std::vector<Item> it;
-    for (int j = 0; j < s.n_ingested * s.G; ++j)
+    for (int j = j0; j < s.n_ingested * s.G; ++j)
       if (s.traj[j].st == L_TS) it.push_back(Item{j, s.traj[j].g, s.grp[s.traj[j].g].v, ctx_len(s, j)});
     return mlq_sort(it);
   };
-  for (int j = 0; j < s.n_ingested * s.G; ++j)
+  for (int j = j0; j < s.n_ingested * s.G; ++j)
     if (s.traj[j].st == L_TS) s.traj[j].ready = t;          // TS-resident: ready now (A18)
   std::vector<Item> mlq = ts_items();
   const int ps = s.ps;                                   // get_ps_version()
@@ -757,6 +770,26 @@ void run_window(Scen &s) {
     else later.push_back(e);
   }
   s.rewards = later;
+  // Deadlock watchdog ("no events pending but steps unfinished", auto trainer only): a
+  // window that made no progress (no decode step, command, completion, Occupy, Consume, publish or
+  // ingest) ending with nothing pending (every instance idle without pending commands or arrivals,
+  // no reward in flight, trainer idle) while groups remain unconsumed is a fixed point; the
+  // scenario fails after wd such windows in a row.
+  if (s.wd > 0 && s.atw > 0) {
+    const int64_t sig = s.m[M_TICKS] + s.m[M_ROUTES] + s.m[M_INTERRUPTS] + s.m[M_PULLS] + s.m[M_COMPLETIONS] +
+                        s.m[M_OCCUPIED] + s.m[M_BATCHES] + s.m[M_PUBLISHES] + s.m[M_INGESTED] + s.m[M_ABORTS];
+    bool pending = s.trainer_busy || !s.rewards.empty();
+    for (const Inst &n : s.inst)
+      pending = pending || n.st != I_IDLE || n.pull_pending || !n.interrupt_set.empty() || !n.abort_set.empty() ||
+                !n.arrivals.empty();
+    const bool work_left = s.live > 0 || s.n_ingested < s.n_pool;
+    if (sig == s.wd_sig && !pending && work_left) {
+      if (++s.wd_idle >= s.wd) s.err = SFO_E_STATE;
+    } else {
+      s.wd_idle = 0;
+    }
+    s.wd_sig = sig;
+  }
   // W9.
   s.t = t_end;
   s.window += 1;
@@ -791,6 +824,7 @@ int sfo_create(int32_t instances, int32_t eta, int32_t group_size, const sfo_con
     s.P = Params{cfg->k1, cfg->k2, cfg->k3, cfg->k4, cfg->k5, cfg->kp, cfg->M,
                  cfg->mu, cfg->phi_tp, cfg->phi_wait, s.eta};
     s.delta = cfg->delta; s.r = cfg->r; s.q = cfg->q; s.R = cfg->R; s.atw = cfg->atw;
+    s.wd = cfg->watchdog_windows;
     s.pool_cap = cfg->pool_capacity_groups;
     s.traj.assign((size_t)s.pool_cap * s.G, Traj());
     s.grp.assign(s.pool_cap, Group());
@@ -831,8 +865,9 @@ int sfo_step(sfo_sim *sim, int32_t n_windows, int32_t n_threads) {
   for (int k = 0; k < ns; ++k) if (sim->sc[k].err) return SFO_E_STATE;
   if (n_threads < 1) n_threads = 1;
   if (n_threads > ns) n_threads = ns;
-  auto work = [&](int tid) {
-    for (int k = tid; k < ns; k += n_threads)
+  std::atomic<int> next{0};                              // scenarios are independent: any order
+  auto work = [&](int) {
+    for (int k = next++; k < ns; k = next++)
       for (int w = 0; w < n_windows; ++w) run_window(sim->sc[k]);
   };
   if (n_threads == 1) work(0);

@@ -43,6 +43,8 @@ typedef struct {
   int32_t pool_capacity_groups;       /* max groups submitted per scenario */
   int32_t extra_groups;               /* batch-level redundancy: buffer slots = B + extra_groups (App C) */
   int32_t extra_members;              /* group-level redundancy: members per group = G + extra_members  */
+  int32_t watchdog_windows;           /* > 0 (auto trainer only): deadlock after this many consecutive windows
+                                         with no progress, nothing pending and work left */
 } sfo_config;
 
 typedef struct sfo_sim sfo_sim;

@@ -25,6 +25,7 @@ struct InstState {
   int st, pullv, pullpend, intkind, intk, cc, v, run_n, whead, wn, arr_n, arr_head;
   int abortn, abortarr;                     // pending Aborts: run/wait members, undelivered arrivals
   int evn;                                  // completion events in this instance's segment (D.iev)
+  int itick;                                // decode steps ended (run_done - itick = remaining)
   long long nb, until, kv, prefill, t_cmd;
   long long ticks, iters, tokens, comps, preempts;
 };
@@ -105,7 +106,7 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
   for (int q = 0; q < kR; ++q) {
     const int s = q * 32 + (int)lane;
     rem[q] = kDead; rid[q] = 0; tq[q] = 0; fin[q] = 0;
-    if (s < x.run_n) { rem[q] = D.run_rem[lb + s]; rid[q] = D.run_id[lb + s]; tq[q] = D.run_T[lb + s]; fin[q] = D.run_fin[lb + s]; }
+    if (s < x.run_n) { rem[q] = D.run_done[lb + s] - x.itick; rid[q] = D.run_id[lb + s]; tq[q] = D.run_T[lb + s]; fin[q] = D.run_fin[lb + s]; }
     live[q] = __ballot_sync(0xffffffffu, s < x.run_n);
   }
   // Arrivals are read through two 32-wide register windows, each refilled with one coalesced
@@ -208,6 +209,7 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
         d[q] = __ballot_sync(0xffffffffu, rem[q] == 0);
         dany |= d[q];
       }
+      x.itick += 1;
       x.kv += k5 * n0;
       x.tokens += n0;
       if (dany) {
@@ -465,6 +467,7 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
         if (m > 0) {
 #pragma unroll
           for (int q = 0; q < kR; ++q) rem[q] -= (int)m;
+          x.itick += (int)m;
           x.nb = (long long)((__int128)x.nb + gm);                   // b_{m+1} = nb + g(m)
           x.kv += m * k5n;
           x.tokens += m * nlive;
@@ -481,6 +484,7 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
           if (one) break;
 #pragma unroll
           for (int q = 0; q < kR; ++q) rem[q] -= 1;
+          x.itick += 1;
           x.kv += k5n;
           x.tokens += nlive;
           x.nb = bq + (long long)P.k1i * (int)x.kv + cn;
@@ -503,7 +507,7 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
   for (int q = 0; q < kR; ++q) {
     if ((live[q] >> lane) & 1u) {
       const int pos = before + __popc(live[q] & lanemask_lt());
-      D.run_rem[lb + pos] = rem[q];
+      D.run_done[lb + pos] = rem[q] + x.itick;
       D.run_id[lb + pos] = rid[q];
       D.run_T[lb + pos] = tq[q];
       D.run_fin[lb + pos] = fin[q];
@@ -541,11 +545,12 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
         int rem = 0, id = 0, Tk = 0, fk = 0;
         bool ab = false;
         if (k < x.run_n) {
-          rem = D.run_rem[lb + k]; id = D.run_id[lb + k]; Tk = D.run_T[lb + k]; fk = D.run_fin[lb + k];
+          rem = D.run_done[lb + k]; id = D.run_id[lb + k]; Tk = D.run_T[lb + k]; fk = D.run_fin[lb + k];
           ab = D.loc[C.traj_off + id] == L_ABORTED;
           if (ab) {
-            release += k5 * (long long)(fk - rem);                                   // p + gen
-            D.gen[C.traj_off + id] = Tk - rem;
+            const int r = rem - x.itick;                                             // remaining
+            release += k5 * (long long)(fk - r);                                     // p + gen
+            D.gen[C.traj_off + id] = Tk - r;
           }
         }
         const bool keep = k < x.run_n && !ab;
@@ -553,7 +558,7 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
         __syncwarp();
         if (keep) {
           const int pos = out + __popc(mk & lanemask_lt());
-          D.run_rem[lb + pos] = rem; D.run_id[lb + pos] = id; D.run_T[lb + pos] = Tk; D.run_fin[lb + pos] = fk;
+          D.run_done[lb + pos] = rem; D.run_id[lb + pos] = id; D.run_T[lb + pos] = Tk; D.run_fin[lb + pos] = fk;
         }
         out += __popc(mk);
         __syncwarp();
@@ -564,21 +569,26 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
       x.abortn = 0;
     }
     if (tick_end) {
+      // one token each: the step count advances; an entry completes when its run_done is reached.
+      // Only the 4-byte run_done is read per entry; entries move (and are rewritten) only behind a
+      // completion
       const int n0 = x.run_n;
+      x.itick += 1;
       int out = 0, ncomp = 0;
       long long release = 0;
       for (int base = 0; base < n0; base += 32) {
         const int k = base + (int)lane;
         const bool valid = k < n0;
-        int rem = 1, id = 0, Tk = 0, fk = 0;
-        if (valid) { rem = D.run_rem[lb + k] - 1; id = D.run_id[lb + k]; Tk = D.run_T[lb + k]; fk = D.run_fin[lb + k]; }
-        const bool done = valid && rem == 0;
+        const int dn = valid ? D.run_done[lb + k] : 0;
+        const bool done = valid && dn == x.itick;
         const bool keep = valid && !done;
         const unsigned mk = __ballot_sync(0xffffffffu, keep);
         const unsigned md = __ballot_sync(0xffffffffu, done);
         const int pos = out + __popc(mk & lanemask_lt());
+        int id = 0, Tk = 0, fk = 0;
+        if (done || (keep && pos != k)) { id = D.run_id[lb + k]; Tk = D.run_T[lb + k]; fk = D.run_fin[lb + k]; }
         __syncwarp();
-        if (keep) { D.run_rem[lb + pos] = rem; D.run_id[lb + pos] = id; D.run_T[lb + pos] = Tk; D.run_fin[lb + pos] = fk; }
+        if (keep && pos != k) { D.run_done[lb + pos] = dn; D.run_id[lb + pos] = id; D.run_T[lb + pos] = Tk; D.run_fin[lb + pos] = fk; }
         if (done) emit_completion(D, C, lb, id, Tk, fk, b, x.evn + ncomp + __popc(md & lanemask_lt()), k5, release);
         out += __popc(mk);
         ncomp += __popc(md);
@@ -598,7 +608,7 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
       const int k = x.run_n - 1;
       const int id = D.run_id[lb + k];
       const long long j = C.traj_off + id;
-      const int rk = D.run_rem[lb + k];
+      const int rk = D.run_done[lb + k] - x.itick;      // remaining
       const int g_ = D.run_T[lb + k] - rk;
       x.kv -= k5 * (long long)(D.run_fin[lb + k] - rk);                         // p + gen
       x.whead = x.whead == 0 ? cap - 1 : x.whead - 1;
@@ -642,7 +652,7 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
       if (lane == 0) {
         const int Tj = D.T[j];
         D.run_id[lb + x.run_n] = id;
-        D.run_rem[lb + x.run_n] = Tj - gj;
+        D.run_done[lb + x.run_n] = x.itick + (Tj - gj);
         D.run_T[lb + x.run_n] = Tj;
         D.run_fin[lb + x.run_n] = (int)(ctx - gj) + Tj;
         D.loc[j] = L_RUN;
@@ -684,6 +694,7 @@ __device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D,
   x.run_n = D.irun_n[gi]; x.whead = D.iwhead[gi]; x.wn = D.iwn[gi];
   x.arr_n = D.iarr_n[gi]; x.arr_head = 0;
   x.abortn = D.iabort[gi]; x.abortarr = D.iabort_arr[gi]; x.evn = D.iev_n[gi];
+  x.itick = D.itick[gi];
   ScenState &SS = D.ss[s];
   const int err0 = SS.err;    // checked below, before the first write
   const int i = gi - C.inst_off;
@@ -717,6 +728,7 @@ __device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D,
     D.ikv[gi] = x.kv; D.iprefill[gi] = x.prefill; D.ic[gi] = x.cc; D.iv[gi] = x.v;
     D.irun_n[gi] = x.run_n; D.iwhead[gi] = x.whead; D.iwn[gi] = x.wn; D.iarr_n[gi] = remain;
     D.iev_n[gi] = x.evn;
+    D.itick[gi] = x.itick;
     if (x.abortn != D.iabort[gi]) D.iabort[gi] = x.abortn;
     if (x.abortarr != D.iabort_arr[gi]) D.iabort_arr[gi] = x.abortarr;
     metric_add(SS, M_TICKS, x.ticks);

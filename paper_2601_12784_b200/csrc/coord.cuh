@@ -711,6 +711,7 @@ static __device__ int interrupt_victims(const GParams &P, const Dev &D, const Sc
   const long long lb = C.list_off + (long long)i * C.cap;
   const long long apply_t = D.ist[gi] == I_TICK ? D.inb[gi] : c.t;
   const int nrun = run_too ? D.irun_n[gi] : 0;
+  const int itk = D.itick[gi];                       // remaining = run_done - itick
   const int whead = D.iwhead[gi];
   const int nvict = nrun + (w_hi - w_lo);
   for (int k0 = 0; k0 < nvict; k0 += 32) {
@@ -720,7 +721,7 @@ static __device__ int interrupt_victims(const GParams &P, const Dev &D, const Sc
       if (k < nrun) {
         id = D.run_id[lb + k];
         const long long j = C.traj_off + id;
-        D.gen[j] = D.T[j] - D.run_rem[lb + k];       // partial progress kept
+        D.gen[j] = D.T[j] - (D.run_done[lb + k] - itk);   // partial progress kept
       } else {
         int pos = whead + w_lo + (k - nrun);
         if (pos >= C.cap) pos -= C.cap;

@@ -135,7 +135,7 @@ __global__ void k_dump_running(GParams P, Dev D, int s, long long *out) {
   const long long lb = C.list_off + (long long)i * C.cap;
   for (int k = threadIdx.x; k < D.irun_n[gi]; k += blockDim.x) {
     const int id = D.run_id[lb + k];
-    out[13LL * id + 4] = D.T[C.traj_off + id] - D.run_rem[lb + k];
+    out[13LL * id + 4] = D.T[C.traj_off + id] - (D.run_done[lb + k] - D.itick[C.inst_off + i]);
   }
 }
 

@@ -323,6 +323,31 @@ __device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, 
     for (int e = np + (int)lane; e < n; e += 32) D.ev_id[C.ev_off + e - np] = tmp[e];
   }
   __syncwarp();
+  // Deadlock watchdog (the oracle's rule, DESIGN.md §4 R-WATCHDOG): no progress in this
+  // window (cumulative progress metrics unchanged), nothing pending at its end, groups unconsumed
+  if (P.wd > 0 && P.atw > 0 && !err) {
+    bool pend = false;
+    for (int i = lane; i < C.I; i += 32) {
+      const long long gi = C.inst_off + i;
+      pend |= D.ist[gi] != I_IDLE || D.ipullpend[gi] != 0 || D.iintkind[gi] != INT_NONE || D.iabort[gi] != 0 ||
+              D.iarr_n[gi] != 0;
+    }
+    pend = __any_sync(0xffffffffu, pend) || SS.trainer_busy || n - np > 0;
+    const long long sig = (long long)(SS.m[M_TICKS] + SS.m[M_ROUTES] + SS.m[M_INTERRUPTS] + SS.m[M_PULLS] +
+                                      SS.m[M_COMPLETIONS] + SS.m[M_OCCUPIED] + m_occ + SS.m[M_BATCHES] +
+                                      SS.m[M_PUBLISHES] + SS.m[M_INGESTED] + SS.m[M_ABORTS] + cl.aborts);
+    const bool work_left = SS.live > 0 || SS.n_ingested < SS.n_pool;
+    __syncwarp();
+    if (lane == 0) {
+      if (sig == SS.wd_sig && !pend && work_left) {
+        if (++SS.wd_idle >= P.wd) err = ERR_DEADLOCK;
+      } else {
+        SS.wd_idle = 0;
+      }
+      SS.wd_sig = sig;
+    }
+    err = __shfl_sync(0xffffffffu, err, 0);
+  }
   if (lane == 0) {
     SS.ev_n = n - np;
     SS.cmd_hash = cl.hash; SS.cmd_n = cl.cmd_n;

@@ -28,6 +28,7 @@ struct sf_ctx {
   int max_inst = 1;
   int fused = 0;                      // launch mode: 1 = one fused window kernel (k_window)
   int pdl = 1;                        // programmatic dependent launch between window kernels
+  int lanes = 0;                      // split mode: one-lane-per-instance advance kernel (SF_ADVANCE=lanes)
   int pdl_mask = 0;                   // debugging (SF_PDL_MASK): bit 0 serializes the advance, bit 1 the ledger
   int dyn = 1;                        // dataflow window kernel (k_dyn.cu)
   int dyn_blocks = 0;
@@ -134,7 +135,11 @@ sf_status check_errors(sf_ctx *c, const long long *m) {
   for (int s = 0; s < c->n_scen; ++s) {
     if (ss[s].err) {
       char buf[160];
-      snprintf(buf, sizeof buf, "scenario %d: invariant violated (code %d) at window %lld", s, ss[s].err, ss[s].window);
+      if (ss[s].err == sf::ERR_DEADLOCK)
+        snprintf(buf, sizeof buf, "scenario %d: deadlock (no progress, nothing pending, work left) at window %lld", s,
+                 ss[s].window);
+      else
+        snprintf(buf, sizeof buf, "scenario %d: invariant violated (code %d) at window %lld", s, ss[s].err, ss[s].window);
       return fail(c, SF_E_STATE, buf);
     }
   }
@@ -193,6 +198,7 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
   P.mu = cfg->mu; P.phi_tp = cfg->phi_throughput; P.phi_wait = cfg->phi_wait;
   P.delta = cfg->snap_period_ps; P.r = cfg->route_lat_ps; P.q = cfg->pull_lat_ps; P.R = cfg->reward_lat_ps;
   P.atw = cfg->auto_train_windows; P.pool_cap = cfg->pool_capacity_groups;
+  P.wd = cfg->watchdog_windows > 0 ? cfg->watchdog_windows : 0;
   P.cmdlog_cap = cfg->command_log_capacity; P.n_scen = ns;
   c->n_scen = ns;
   c->hsc.resize(ns);
@@ -206,15 +212,24 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
     S.I = cfg->scenario_instances ? cfg->scenario_instances[s] : instances;
     S.eta = cfg->scenario_eta ? cfg->scenario_eta[s] : eta;
     S.strategy = (int)(cfg->scenario_strategy ? cfg->scenario_strategy[s] : cfg->strategy);
-    if (S.I < 1 || S.I > sf::kMaxInst || S.eta < 0 || S.eta > sf::kMaxEta || pool_traj >= (1LL << 27)) {
+    // grp_of() (sf_internal.cuh): id * gmag must fit in 64 bits for every id < pool_traj, and the
+    // multiply-shift is exact for id < 2^40 / G (both follow from this check for G <= 4096)
+    const bool grp_ok = pool_traj < (1LL << 27) &&
+                        ((unsigned __int128)(unsigned long long)(pool_traj - 1) * P.gmag >> 64) == 0 &&
+                        (pool_traj - 1) < (long long)((1ULL << 40) / (unsigned long long)G);
+    if (S.I < 1 || S.I > sf::kMaxInst || S.eta < 0 || S.eta > sf::kMaxEta || !grp_ok) {
       delete c;
       return SF_E_INVALID;
     }
-    S.cap = (S.eta + 1) * B * G;
-    if ((long long)S.I * S.cap >= (1LL << 31)) {          // 32-bit per-scenario list offsets
+    const long long cap64 = (long long)(S.eta + 1) * B * G;
+    // every per-scenario offset below is narrowed to int (or indexes int-sized lists): reject any
+    // configuration whose offsets reach 2^31 before narrowing
+    if (cap64 * S.I >= (1LL << 31) || (long long)(s + 1) * P.pool_cap >= (1LL << 31) ||
+        inst + S.I >= (1LL << 31) || led + (long long)(S.eta + 1) * B >= (1LL << 31) || ring + S.eta + 1 >= (1LL << 31)) {
       delete c;
       return SF_E_INVALID;
     }
+    S.cap = (int)cap64;
     S.inst_off = (int)inst; S.grp_off = s * P.pool_cap; S.led_off = (int)led; S.ring_off = (int)ring;
     S.traj_off = (long long)s * pool_traj; S.list_off = list; S.bits_off = bits; S.mlq_off = mlq;
     S.ev_off = ev; S.batch_off = batch; S.cmd_off = cmd;
@@ -237,7 +252,14 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
   if (const char *m = getenv("SF_PDL_MASK")) c->pdl_mask = atoi(m);
   c->P.pdl = 0;
   c->P.epoch = 0;
-  if (const char *m = getenv("SF_ADVANCE")) c->P.skip = strcmp(m, "step") != 0;
+  // decode-advance kernel: one warp per instance with closed-form quiet steps by
+  // default; SF_ADVANCE=step the same one step at a time; SF_ADVANCE=lanes one lane per instance
+  // (advance_lanes.cuh; bit-exact, measured slower on C5)
+  c->lanes = 0;
+  if (const char *m = getenv("SF_ADVANCE")) {
+    c->P.skip = strcmp(m, "step") != 0;
+    c->lanes = strcmp(m, "lanes") == 0;
+  }
   if (const char *m = getenv("SF_LAUNCH")) {
     if (!strcmp(m, "split")) { c->fused = 0; c->dyn = 0; }
     if (!strcmp(m, "fused")) { c->fused = c->max_inst <= 32; c->dyn = 0; }
@@ -273,7 +295,7 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
   }
   ok = ok && dalloc(c, &D.run_T, list, 0) && dalloc(c, &D.run_fin, list, 0) && dalloc(c, &D.iev, list, 0) &&
        dalloc(c, &D.iev_n, inst, 0);
-  ok = ok && dalloc(c, &D.run_id, list, 0) && dalloc(c, &D.run_rem, list, 0) && dalloc(c, &D.wait_id, list, 0) &&
+  ok = ok && dalloc(c, &D.run_id, list, 0) && dalloc(c, &D.run_done, list, 0) && dalloc(c, &D.itick, inst, 0) && dalloc(c, &D.wait_id, list, 0) &&
        dalloc(c, &D.arr_id, list, 0) && dalloc(c, &D.arr_t, list, 0);
   ok = ok && dalloc(c, &D.led_st, led, 0) && dalloc(c, &D.led_g, led, 0xFF) && dalloc(c, &D.led_v, led, 0xFF) &&
        dalloc(c, &D.led_nres, ring, 0) && dalloc(c, &D.led_nocc, ring, 0);
@@ -450,7 +472,8 @@ sf_status sf_step(sf_ctx *c, int32_t n_windows, sf_step_stats *out) {
     prof_mark(c, 0);
     P.pdl = pdl && !(c->pdl_mask & 1);
     prof_mark(c, 1);
-    sf_launch_advance(P, c->D, c->n_inst_total, c->stream);
+    if (c->lanes) sf_launch_advance_lanes(P, c->D, c->n_inst_total, c->stream);
+    else sf_launch_advance(P, c->D, c->n_inst_total, c->stream);
     prof_mark(c, 1);
     P.pdl = pdl && !(c->pdl_mask & 2);
     prof_mark(c, 2);

@@ -42,7 +42,7 @@ class SfConfig(C.Structure):
         ("snap_period_ps", C.c_int64), ("route_lat_ps", C.c_int64), ("pull_lat_ps", C.c_int64),
         ("reward_lat_ps", C.c_int64), ("strategy", C.c_uint32), ("auto_train_windows", C.c_int32),
         ("pool_capacity_groups", C.c_int32), ("command_log_capacity", C.c_int32),
-        ("extra_groups", C.c_int32), ("extra_members", C.c_int32),
+        ("extra_groups", C.c_int32), ("extra_members", C.c_int32), ("watchdog_windows", C.c_int32),
         ("device", C.c_int32), ("cuda_stream", C.c_void_p),
     ]
 
@@ -125,7 +125,8 @@ class StaleFlow:
                  phi_wait: int = W.PHI_WAIT, snap_period: int = W.PS_PER_S, route_lat: int = 10_000_000_000,
                  pull_lat: int = 2 * W.PS_PER_S, reward_lat: int = W.PS_PER_S, strategy: int = W.STRAT_SF,
                  auto_train_windows: int = 0, pool_capacity_groups: int = 1024, command_log_capacity: int = 0,
-                 extra_groups: int = 0, extra_members: int = 0, device: Optional[int] = None, stream=None):
+                 extra_groups: int = 0, extra_members: int = 0, watchdog_windows: int = 0,
+                 device: Optional[int] = None, stream=None):
         import torch  # device + stream plumbing only
         if not torch.cuda.is_available():
             raise SfError("StaleFlow needs a CUDA device (no CPU fallback)")
@@ -143,6 +144,8 @@ class StaleFlow:
             if x is None:
                 return None
             a = np.ascontiguousarray(np.asarray(x, dtype=dt))
+            if a.shape != (n_scenarios,):
+                raise SfError(f"per-scenario array of shape {a.shape}, expected ({n_scenarios},)")
             self._keep.append(a)
             return _p(a, ct)
 
@@ -155,7 +158,8 @@ class StaleFlow:
                        snap_period_ps=snap_period, route_lat_ps=route_lat, pull_lat_ps=pull_lat,
                        reward_lat_ps=reward_lat, strategy=strategy, auto_train_windows=auto_train_windows,
                        pool_capacity_groups=pool_capacity_groups, command_log_capacity=command_log_capacity,
-                       extra_groups=extra_groups, extra_members=extra_members, device=device, cuda_stream=C.c_void_p(stream.cuda_stream))
+                       extra_groups=extra_groups, extra_members=extra_members, watchdog_windows=watchdog_windows,
+                       device=device, cuda_stream=C.c_void_p(stream.cuda_stream))
         self.h = C.c_void_p()
         rc = self.L.sf_create(instances, eta, group_size, C.byref(cfg), C.byref(self.h))
         if rc != 0:
@@ -191,19 +195,38 @@ class StaleFlow:
             raise SfError(f"{what}: {STATUS.get(rc, rc)}: {self.L.sf_last_error(self.h).decode()}")
         return rc
 
+    def _status(self, rc, what):
+        """Calls whose documented failures leave the context usable (submit, publish, collect) return
+        their sf_status for the caller to test; a poisoning status (SF_E_STATE, SF_E_NOMEM, SF_E_CUDA)
+        raises, so a failure that ends the context cannot go unnoticed."""
+        if rc in (-3, -4, -5):
+            self._check(rc, what)
+        return rc
+
     # ------------------------------------------------------------------ API
     def submit(self, scen: int, prompt, target) -> int:
-        prompt = np.ascontiguousarray(prompt, dtype=np.int32)
-        target = np.ascontiguousarray(target, dtype=np.int32)
-        return self.L.sf_submit_prompts(self.h, scen, len(prompt), _p(prompt, C.c_int32), _p(target, C.c_int32))
+        """sf_submit_prompts: prompt[n_groups], target[n_groups * members] (members = G + extra)."""
+        prompt = np.ascontiguousarray(prompt, dtype=np.int32).reshape(-1)
+        target = np.ascontiguousarray(target, dtype=np.int32).reshape(-1)
+        if target.size != prompt.size * self.members:
+            raise SfError(f"submit: {target.size} targets for {prompt.size} groups of {self.members} members")
+        return self._status(self.L.sf_submit_prompts(self.h, scen, len(prompt), _p(prompt, C.c_int32),
+                                                     _p(target, C.c_int32)), "sf_submit_prompts")
 
     def submit_many(self, scen_ids, n_groups, prompts, targets) -> int:
-        a = np.ascontiguousarray(scen_ids, dtype=np.int32)
-        b = np.ascontiguousarray(n_groups, dtype=np.int32)
-        pr = np.ascontiguousarray(prompts, dtype=np.int32)
-        tg = np.ascontiguousarray(targets, dtype=np.int32)
-        return self.L.sf_submit_prompts_many(self.h, len(a), _p(a, C.c_int32), _p(b, C.c_int32),
-                                             _p(pr, C.c_int32), _p(tg, C.c_int32))
+        """sf_submit_prompts_many: scen_ids[n], n_groups[n]; prompts[sum n_groups] and
+        targets[sum n_groups * members] concatenated in scenario order."""
+        a = np.ascontiguousarray(scen_ids, dtype=np.int32).reshape(-1)
+        b = np.ascontiguousarray(n_groups, dtype=np.int32).reshape(-1)
+        pr = np.ascontiguousarray(prompts, dtype=np.int32).reshape(-1)
+        tg = np.ascontiguousarray(targets, dtype=np.int32).reshape(-1)
+        tot = int(b.astype(np.int64).sum())
+        if a.size != b.size or (b < 0).any() or pr.size != tot or tg.size != tot * self.members:
+            raise SfError(f"submit_many: {a.size} scenario ids, {b.size} counts (sum {tot}), {pr.size} prompts, "
+                          f"{tg.size} targets for {self.members} members per group")
+        return self._status(self.L.sf_submit_prompts_many(self.h, len(a), _p(a, C.c_int32), _p(b, C.c_int32),
+                                                          _p(pr, C.c_int32), _p(tg, C.c_int32)),
+                            "sf_submit_prompts_many")
 
     def submit_many_ptr(self, n, scen_ptr, ng_ptr, prompt_ptr, target_ptr) -> int:
         """Raw host pointers (e.g. pinned torch tensors' data_ptr())."""
@@ -220,7 +243,7 @@ class StaleFlow:
         return None
 
     def publish(self, scen: int, version: int) -> int:
-        return self.L.sf_publish_params(self.h, scen, version)
+        return self._status(self.L.sf_publish_params(self.h, scen, version), "sf_publish_params")
 
     def collect(self, scen: int):
         B = self.B
@@ -230,7 +253,7 @@ class StaleFlow:
         n = np.zeros(1, np.int32)
         rc = self.L.sf_collect_batch(self.h, scen, B, _p(vb, C.c_int32), _p(g, C.c_int32), _p(v, C.c_int32),
                                      _p(n, C.c_int32))
-        return rc, int(vb[0]), g, v
+        return self._status(rc, "sf_collect_batch"), int(vb[0]), g, v
 
     def mark_filtered(self, scen: int, first_group: int, flags) -> None:
         """Filtering (P:413 (2)): flags[a] != 0 drops group first_group + a when it completes."""

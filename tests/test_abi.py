@@ -77,10 +77,13 @@ def test_oracle_is_independent_of_the_product():
 
 
 def test_group_division_multiply_shift_exact():
-    """grp_of() (sf_internal.cuh): id / G == (id * ceil(2^40/G)) >> 40 for id < 2^27, G <= 4096."""
+    """grp_of() (sf_internal.cuh): id / G == (id * ceil(2^40/G)) >> 40 in 64-bit arithmetic for every id
+    sf_create accepts: id < 2^27, id * m < 2^64 (G = 1 with 2^24 trajectories would wrap)."""
     import random
     rng = random.Random(7)
     for G in list(range(1, 65)) + [96, 100, 1000, 4095, 4096]:
         m = ((1 << 40) + G - 1) // G
-        ids = list(range(5000)) + [rng.randrange(1 << 27) for _ in range(5000)] + [(1 << 27) - 1 - k for k in range(500)]
-        assert all((i * m) >> 40 == i // G for i in ids), G
+        top = min(1 << 27, ((1 << 64) - 1) // m + 1)         # sf_create: pool_traj - 1 < top
+        ids = list(range(5000)) + [rng.randrange(top) for _ in range(5000)] + [top - 1 - k for k in range(500)]
+        assert all((i * m) < (1 << 64) and ((i * m) & ((1 << 64) - 1)) >> 40 == i // G for i in ids), G
+    assert (((1 << 24) * (1 << 40)) & ((1 << 64) - 1)) >> 40 == 0   # the wrap sf_create now rejects (G = 1)

@@ -84,7 +84,13 @@ def make(**kw):
 @pytest.mark.parametrize("bad", [dict(batch_size=0), dict(group_size=0), dict(group_size=5000), dict(eta=16),
                                  dict(instances=129), dict(kv_budget=1 << 30), dict(k1=1 << 31), dict(k5=0),
                                  dict(snap_period=0), dict(pool_capacity_groups=0), dict(extra_groups=-1),
-                                 dict(extra_members=-1)])
+                                 dict(extra_members=-1),
+                                 # grp_of()'s 64-bit multiply-shift would wrap: G = 1 beyond 2^24
+                                 # trajectories, G = 3 beyond ~3 * 2^24
+                                 dict(group_size=1, pool_capacity_groups=(1 << 24) + 1),
+                                 dict(group_size=3, pool_capacity_groups=(1 << 24) + 1),
+                                 # per-scenario list offsets would pass 2^31 (cap = (eta+1) B G in int64)
+                                 dict(eta=15, batch_size=1 << 16, group_size=4096, pool_capacity_groups=1)])
 def test_create_rejects_invalid_config(bad):
     from paper_2601_12784_b200.staleflow import SfError
     with pytest.raises(SfError):
@@ -111,3 +117,36 @@ def test_call_errors_do_not_poison():
     assert out[0] == 2                                                            # *n_out = B
     ctx.step(3)                                                                   # still usable
     assert ctx.metrics()[0] == 3
+
+
+def test_binding_rejects_mismatched_shapes():
+    """The binding checks array sizes before handing host pointers to the C ABI: a short
+    target array would otherwise be over-read by sf_submit_prompts[_many]."""
+    from paper_2601_12784_b200.staleflow import SfError
+    ctx = make(extra_members=1)                          # 3 members per group
+    p = np.array([10, 10], np.int32)
+    with pytest.raises(SfError):
+        ctx.submit(0, p, np.full(4, 5, np.int32))        # 2 groups x 2 members: one member short per group
+    with pytest.raises(SfError):
+        ctx.submit_many([0], [2], p, np.full(4, 5, np.int32))
+    with pytest.raises(SfError):
+        ctx.submit_many([0, 0], [2], p, np.full(6, 5, np.int32))
+    assert ctx.submit(0, p, np.full(6, 5, np.int32)) == OK
+
+
+def test_watchdog_deadlock_matches_oracle():
+    """SPEC S:494 Deadlock: the hand-derived starved batch of tests/test_oracle_pins.py on the GPU: the
+    library poisons the scenario in the same window as the oracle and sf_step returns SF_E_STATE."""
+    from paper_2601_12784_b200.staleflow import SfError
+    from tests.test_oracle_pins import watchdog_sim
+    o = watchdog_sim(3)
+    g2 = make(instances=1, eta=0, group_size=1, batch_size=2, kv_budget=1000, pool_capacity_groups=2,
+              auto_train_windows=1, watchdog_windows=3)
+    assert g2.submit(0, np.array([10], np.int32), np.array([2], np.int32)) == OK
+    g2.step(3, stats=True)
+    with pytest.raises(SfError, match="deadlock .* at window 4"):
+        g2.step(1, stats=True)                  # a synchronizing call reports the poisoned scenario
+    assert o.step(3) == 0 and o.step(1) == E_STATE
+    assert o.metrics(0)[0] == 4                 # the oracle fails in the same window (4 windows run)
+    with pytest.raises(SfError):                # the context is poisoned (include/staleflow.h)
+        g2.metrics(0)

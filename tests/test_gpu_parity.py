@@ -16,11 +16,12 @@ from tests.parity import compare, make_pair, run_lockstep, submit_both
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["auto", "fused", "step", "dyn", "nopdl"])
+@pytest.fixture(params=["auto", "lanes", "fused", "step", "dyn", "nopdl"])
 def launch_mode(request, monkeypatch):
     """Every launch / decode-step mode must give identical results: default (three kernels with
-    programmatic dependent launch, closed-form quiet steps), fused window kernel, one-by-one
-    decode steps, the dataflow window kernel, and three fully serialized kernels."""
+    programmatic dependent launch, one warp per instance and closed-form quiet steps in the
+    advance), the one-lane-per-instance advance, fused window kernel, one-by-one decode steps, the
+    dataflow window kernel, and three fully serialized kernels."""
     monkeypatch.delenv("SF_LAUNCH", raising=False)
     monkeypatch.delenv("SF_ADVANCE", raising=False)
     monkeypatch.delenv("SF_PDL", raising=False)
@@ -32,6 +33,8 @@ def launch_mode(request, monkeypatch):
         monkeypatch.setenv("SF_LAUNCH", "fused")
     if request.param == "step":
         monkeypatch.setenv("SF_ADVANCE", "step")
+    if request.param == "lanes":
+        monkeypatch.setenv("SF_ADVANCE", "lanes")
     return request.param
 
 

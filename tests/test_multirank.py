@@ -1,8 +1,8 @@
 """World-size-2 test of the multi-GPU host logic on CPU (gloo): scenario sharding (bench.shard,
-weak scaling) and the metrics all-reduce (bench.reduce_metrics) must reproduce, bit for bit,
-the metrics of one process running every scenario (integer sums, max time).
-The per-rank simulation runs in the oracle here (no GPU on this box); on a GPU box bench.py
-runs the same host logic over NCCL with the CUDA library."""
+scenario s -> rank s mod W) and the metrics all-reduce (bench.reduce_metrics) must
+reproduce, bit for bit, the metrics of one process running every scenario (integer
+sums, max time).  The per-rank simulation runs in the oracle here (no GPU on this box);
+tests/test_gpu_multirank.py runs the same host logic over NCCL with the CUDA library on 2 GPUs."""
 import os
 import socket
 
@@ -30,7 +30,7 @@ def _run_rank(rank, world, port, out_path):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     full = W.preset("C5", n_scenarios=S_PER_RANK * world)
-    idx = bench.shard(S_PER_RANK, rank)
+    idx = bench.shard(full, rank, world, "weak")
     o = OracleSim.from_preset(full, idx)
     for a, k in enumerate(idx):
         pr, tg = W.draw_lengths(full, k, full.pool_groups)
@@ -61,6 +61,11 @@ def test_two_rank_gloo_metrics_equal_single_process(tmp_path):
 
 
 def test_shards_partition_the_family():
-    S, world = 4096, 8
-    seen = sorted(k for r in range(world) for k in bench.shard(S, r))
-    assert seen == list(range(S * world))
+    for S, world, mode in ((4096, 8, "weak"), (4096, 8, "strong"), (50, 4, "strong")):
+        full = W.preset("C5", n_scenarios=S * (world if mode == "weak" else 1))
+        parts = [bench.shard(full, r, world, mode) for r in range(world)]
+        assert sorted(k for p in parts for k in p) == list(range(len(full.scenarios)))
+        assert all(k % world == r for r, p in enumerate(parts) for k in p)            # s mod W
+        assert max(map(len, parts)) - min(map(len, parts)) <= 1
+    c3 = W.preset("C3")                                                             # replicas
+    assert all(bench.shard(c3, r, 4, "replicas") == [0] for r in range(4))

@@ -115,3 +115,43 @@ def test_cascade_lowest_slot_within_buffer():
         assert L.reserve(g, 0)[1:] == where
     assert L.delete_relocate(0) == 1
     assert L.entries(2) == [[("Empty", -1, -1), ("Reserved", 2, 0)], [("Reserved", 1, 0), ("Reserved", 3, 0)]]
+
+
+def watchdog_sim(wd):
+    """Hand-derived: I=1, eta=0, B=2, G=1, one group (p10, T2) in the pool, auto trainer.  Window 0
+    routes, decodes and completes it (Occupy buffer 0 slot 0); the batch needs a second group that
+    never comes, so from window 1 on nothing progresses and nothing is pending while a live group
+    remains: windows 1, 2, 3 are idle and the watchdog (wd = 3) fails the scenario at window 3."""
+    cfg = Config(batch_size=2, n_scenarios=1, k1=1, k2=100, k3=10, k4=50, k5=1, kp=0, M=1000, mu=0.3,
+                 phi_tp=5.0, phi_wait=3, delta=1000, r=5, q=30, R=20, strategy=7, atw=1, pool_capacity_groups=2,
+                 watchdog_windows=wd)
+    s = OracleSim(1, 0, 1, cfg)
+    assert s.submit(0, np.array([10]), np.array([2])) == 0
+    return s
+
+
+def test_watchdog_deadlock_starved_batch():
+    """SPEC S:494 Deadlock ("no events pending but steps unfinished")."""
+    s = watchdog_sim(3)
+    assert s.step(3) == 0
+    assert s.metrics()[IDX["occupied_groups"]] == 1 and s.metrics()[IDX["batches"]] == 0
+    assert s.step(1) == -3                                      # SFO_E_STATE in window 3
+    m = s.metrics()
+    assert m[IDX["poisoned_scenarios"]] == 1 and m[IDX["windows"]] == 4
+    off = watchdog_sim(0)                                       # off: idles forever, no error
+    assert off.step(50) == 0 and off.metrics()[IDX["poisoned_scenarios"]] == 0
+
+
+def test_watchdog_never_fires_on_progressing_runs():
+    """A watchdog of 1 window leaves every normal simulation alone: each window either progresses or
+    has something pending until all work is consumed (transcription configs, full length)."""
+    import random
+    from tests.test_oracle_fraction import tiny_config
+    for seed in range(60):
+        rng = random.Random(seed)
+        I, eta, G, B, kw, prompt, target = tiny_config(rng)
+        # pool = whole batches only (a partial last batch would legitimately starve)
+        cfg = Config(batch_size=B, n_scenarios=1, pool_capacity_groups=len(prompt), watchdog_windows=1, **kw)
+        s = OracleSim(I, eta, G, cfg)
+        assert s.submit(0, prompt, target) == 0
+        assert s.step(200) == 0, f"seed {seed}: watchdog fired"

@@ -67,6 +67,16 @@ for lo, hi in ((0, 0), (1, 8), (9, 64), (65, 200), (201, 10 ** 9)):
         print(f"routes in [{lo},{hi}]: {m.mean():.3f} of scenario-windows, {tot[m].sum() / tot.sum():.3f} of cycles, "
               f"median {np.median(tot[m]):.0f} cycles, {np.median(ph[m, 4] / np.maximum(r[m], 1)):.0f} routing cycles/route")
 ad = np.concatenate(arow)
+if os.environ.get("SF_ADVANCE", "") not in ("warp", "step"):
+    # one-lane-per-instance kernel (advance_lanes.cuh): loop, stage, coordinator wait, tail cycles,
+    # warp iterations, arrival-window refills, wait heads read from HBM, arrivals per lane
+    print(f"== advance (lanes), {4 * n} instances per window")
+    for k, name in enumerate(["loop", "stage", "wait", "tail", "iterations", "refills", "head_hbm", "arrivals"]):
+        v = ad[:, k]
+        print(f"  {name:10s} p50 {np.percentile(v, 50):9.0f} p90 {np.percentile(v, 90):9.0f} max {v.max():9.0f} mean {v.mean():9.1f}")
+    X = np.stack([np.ones(len(ad)), ad[:, 4]], 1).astype(np.float64)
+    print("  loop cycles ~ %.0f + %.0f per warp iteration" % tuple(np.linalg.lstsq(X, ad[:, 0].astype(np.float64), rcond=None)[0]))
+    sys.exit(0)
 cyc = ad[:, 0]
 print(f"== advance, {4 * n} instances per window")
 print("cycles per instance-window: p50 %.0f p90 %.0f p99 %.0f max %.0f; mean %.0f" % (
