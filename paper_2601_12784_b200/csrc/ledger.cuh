@@ -172,14 +172,64 @@ static __device__ void filter_group(const GParams &P, const Dev &D, const ScenCo
   __syncwarp();
 }
 
-constexpr int kEvStage = 256;     // reward events staged per warp in shared memory
+constexpr int kEvStage = 512;     // reward events staged per warp in shared memory (a power of two)
 
 struct EvStage {
   long long t[kEvStage];
   int id[kEvStage];
-  int srt[kEvStage];
   int ioff[kMaxInst + 1];         // start of each instance's events in the window's event order
 };
+
+// (t, id) < (t', id'): the order in which reward events reach the ledger (W8)
+__device__ __forceinline__ bool ev_less(long long ta, int ia, long long tb, int ib) {
+  return (ta < tb) | ((ta == tb) & (ia < ib));
+}
+
+// bitonic sort of n <= kEvStage staged events by (t, id), in shared memory (padded to a power of two
+// with (+inf, +inf); keys are distinct); O(N log^2 N / 32) compare-exchanges per lane
+__device__ __forceinline__ void ev_sort_smem(EvStage &es, int n) {
+  int N = 1;
+  while (N < n) N <<= 1;
+  for (int e = n + (int)lane_id(); e < N; e += 32) { es.t[e] = 0x7fffffffffffffffLL; es.id[e] = 0x7fffffff; }
+  __syncwarp();
+  for (int k = 2; k <= N; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane_id(); i < N; i += 32) {
+        const int p = i ^ j;
+        if (p > i) {
+          const long long ta = es.t[i], tb = es.t[p];
+          const int ia = es.id[i], ib = es.id[p];
+          const bool up = (i & k) == 0;
+          if (ev_less(tb, ib, ta, ia) == up) { es.t[i] = tb; es.t[p] = ta; es.id[i] = ib; es.id[p] = ia; }
+        }
+      }
+      __syncwarp();
+    }
+}
+
+// the same network over event ids in global scratch (n > kEvStage, rare), keyed by
+// (D.t_complete[id], id); padding ids are -1 (= +inf)
+__device__ __forceinline__ void ev_sort_global(const Dev &D, const ScenConst &C, int *ids, int n) {
+  int N = 1;
+  while (N < n) N <<= 1;
+  for (int e = n + (int)lane_id(); e < N; e += 32) ids[e] = -1;
+  __syncwarp();
+  auto key_t = [&](int id) { return id < 0 ? 0x7fffffffffffffffLL : D.t_complete[C.traj_off + id]; };
+  for (int k = 2; k <= N; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane_id(); i < N; i += 32) {
+        const int p = i ^ j;
+        if (p > i) {
+          const int ia = ids[i], ib = ids[p];
+          const long long ta = key_t(ia), tb = key_t(ib);
+          const bool up = (i & k) == 0;
+          const bool b_lt_a = ev_less(tb, ib < 0 ? 0x7fffffff : ib, ta, ia < 0 ? 0x7fffffff : ia);
+          if (b_lt_a == up) { ids[i] = ib; ids[p] = ia; }
+        }
+      }
+      __syncwarp();
+    }
+}
 
 // One window of W8-W9 for scenario s, executed by one warp (es: that warp's staging).
 // C = D.sc[s] (passed in, loaded by the caller before its wait).
@@ -211,13 +261,16 @@ __device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, 
     }
     return lo;
   };
-  if (n > kEvStage) {                             // rare: gather the segments into the carry list
-    for (int e = n_carry + (int)lane; e < n; e += 32) {
-      const int i = seg_of(e);
-      D.ev_id[C.ev_off + e] = D.iev[C.list_off + (long long)i * C.cap + (e - es.ioff[i])];
-    }
-    __syncwarp();
+  const bool big = n > kEvStage;                  // rare: the events do not fit the staging
+  int *gids = D.mlq + C.mlq_off;                  // big: ids sorted in the MLQ scratch (>= 3 cap ints)
+  for (int e = lane; e < n; e += 32) {
+    int id;
+    if (e < n_carry) id = D.ev_id[C.ev_off + e];
+    else { const int i = seg_of(e); id = D.iev[C.list_off + (long long)i * C.cap + (e - es.ioff[i])]; }
+    if (big) gids[e] = id;
+    else { es.id[e] = id; es.t[e] = D.t_complete[C.traj_off + id]; }
   }
+  __syncwarp();
   for (int i = lane; i < C.I; i += 32) D.iev_n[C.inst_off + i] = 0;
 #ifdef SF_CHECK
   assert(n >= 0 && n <= C.cap);
@@ -227,101 +280,47 @@ __device__ __forceinline__ void ledger_scenario(const GParams &P, const Dev &D, 
   long long m_reloc = 0, m_occ = 0;
   CmdLog cl{SS.cmd_hash, SS.cmd_n, SS.window, 0};
   int np = 0;
-  if (n <= kEvStage) {
-    // stage (t_complete, id), rank-sort by (t_reward, id) (W8) in shared memory
-    for (int e = lane; e < n; e += 32) {
-      int id;
-      if (e < n_carry) id = D.ev_id[C.ev_off + e];
-      else { const int i = seg_of(e); id = D.iev[C.list_off + (long long)i * C.cap + (e - es.ioff[i])]; }
-      es.id[e] = id;
-      es.t[e] = D.t_complete[C.traj_off + id];
-    }
+  // sort by (t_reward, id) = (t_complete + R, id) (W8)
+  if (big) ev_sort_global(D, C, gids, n);
+  else ev_sort_smem(es, n);
+  auto ev_id = [&](int k) { return big ? gids[k] : es.id[k]; };
+  // apply in order, 32 events per batch: the members' reward counters are loaded in parallel and
+  // same-group events inside a batch are counted with __match_any_sync
+  for (int k0 = 0; k0 < n; k0 += 32) {
+    const int k = k0 + (int)lane;
+    const bool valid = k < n;
+    const int id = valid ? ev_id(k) : 0;
+    const long long te = valid ? (big ? D.t_complete[C.traj_off + id] : es.t[k]) : 0;
+    const bool ok = valid && te + P.R <= t_end;
+    const int g = grp_of(P, id);
+    const unsigned okm = __ballot_sync(0xffffffffu, ok);
+    // redundancy: the reward of an aborted member is ignored, and inside this batch the
+    // members of a group past its Gr-th reward are aborted when the group completes
+    bool eff = ok;
+    if (P.abortable && ok) eff = D.loc[C.traj_off + id] != L_ABORTED;
+    const int nrw = eff ? D.n_rew[C.grp_off + g] : 0;
+    const unsigned same = __match_any_sync(0xffffffffu, eff ? g : -1 - (int)lane);
+    const int nr = nrw + 1 + __popc(same & lanemask_lt());
+    if (eff && (same >> lane) == 1u) D.n_rew[C.grp_off + g] = min(nrw + __popc(same), P.Gr);   // last of its group
+    if (P.red && eff && nr <= P.Gr) D.loc[C.traj_off + id] = L_REWARDED;
+    unsigned cm = __ballot_sync(0xffffffffu, eff && nr == P.Gr);
     __syncwarp();
-    for (int e = lane; e < n; e += 32) {
-      const long long te = es.t[e];
-      const int ie = es.id[e];
-      int rank = 0;
-#pragma unroll 4
-      for (int f = 0; f < n; ++f) {                      // branch-free compare (no divergence)
-        const long long tf = es.t[f];
-        const int jf = es.id[f];
-        rank += (int)((tf < te) | ((tf == te) & (jf < ie)));
-      }
-      es.srt[rank] = e;
+    while (cm) {
+      const int l = __ffs(cm) - 1;
+      cm &= cm - 1;
+      const int gc = __shfl_sync(0xffffffffu, g, l);
+      if (P.red)                                      // group-level redundancy: Abort the others
+        for (int m = 0; m < P.G; ++m) abort_member(P, D, C, cl, gc * P.G + m);
+      if (P.filt && D.gfilt[C.grp_off + gc]) filter_group(P, D, C, SS, gc, cu, cl, m_reloc, err);
+      else complete_group(P, D, C, SS, gc, cu, m_reloc, m_occ, err);
+      if (err) break;
     }
-    __syncwarp();
-    // apply in order, 32 events per batch: the members' reward counters are loaded in parallel and
-    // same-group events inside a batch are counted with __match_any_sync
-    for (int k0 = 0; k0 < n; k0 += 32) {
-      const int k = k0 + (int)lane;
-      const bool valid = k < n;
-      const int e = valid ? es.srt[k] : 0;
-      const int id = es.id[e];
-      const bool ok = valid && es.t[e] + P.R <= t_end;
-      const int g = grp_of(P, id);
-      const unsigned okm = __ballot_sync(0xffffffffu, ok);
-      // redundancy: the reward of an aborted member is ignored, and inside this batch the
-      // members of a group past its Gr-th reward are aborted when the group completes
-      bool eff = ok;
-      if (P.abortable && ok) eff = D.loc[C.traj_off + id] != L_ABORTED;
-      const int nrw = eff ? D.n_rew[C.grp_off + g] : 0;
-      const unsigned same = __match_any_sync(0xffffffffu, eff ? g : -1 - (int)lane);
-      const int nr = nrw + 1 + __popc(same & lanemask_lt());
-      if (eff && (same >> lane) == 1u) D.n_rew[C.grp_off + g] = min(nrw + __popc(same), P.Gr);   // last of its group
-      if (P.red && eff && nr <= P.Gr) D.loc[C.traj_off + id] = L_REWARDED;
-      unsigned cm = __ballot_sync(0xffffffffu, eff && nr == P.Gr);
-      __syncwarp();
-      while (cm) {
-        const int l = __ffs(cm) - 1;
-        cm &= cm - 1;
-        const int gc = __shfl_sync(0xffffffffu, g, l);
-        if (P.red)                                      // group-level redundancy: Abort the others
-          for (int m = 0; m < P.G; ++m) abort_member(P, D, C, cl, gc * P.G + m);
-        if (P.filt && D.gfilt[C.grp_off + gc]) filter_group(P, D, C, SS, gc, cu, cl, m_reloc, err);
-        else complete_group(P, D, C, SS, gc, cu, m_reloc, m_occ, err);
-        if (err) break;
-      }
-      np += __popc(okm);
-      if (err || okm != __ballot_sync(0xffffffffu, valid)) break;   // sorted: the rest are later
-    }
-    __syncwarp();
-    for (int k = np + (int)lane; k < n; k += 32) D.ev_id[C.ev_off + k - np] = es.id[es.srt[k]];
-  } else {
-    int *tmp = D.mlq + C.mlq_off;                     // scratch (the MLQ is rebuilt per cycle)
-    for (int e = lane; e < n; e += 32) {
-      const int ie = D.ev_id[C.ev_off + e];
-      const long long te = D.t_complete[C.traj_off + ie];
-      int rank = 0;
-      for (int f = 0; f < n; ++f) {
-        const int jf = D.ev_id[C.ev_off + f];
-        const long long tf = D.t_complete[C.traj_off + jf];
-        rank += (tf < te) || (tf == te && jf < ie);
-      }
-      tmp[rank] = ie;
-    }
-    __syncwarp();
-    for (; np < n; ++np) {
-      const int id = tmp[np];
-      if (D.t_complete[C.traj_off + id] + P.R > t_end) break;
-      const int g = grp_of(P, id);
-      if (P.abortable && D.loc[C.traj_off + id] == L_ABORTED) continue;     // ignored reward
-      const int nr = D.n_rew[C.grp_off + g] + 1;
-      __syncwarp();
-      if (lane == 0) {
-        D.n_rew[C.grp_off + g] = nr;
-        if (P.red) D.loc[C.traj_off + id] = L_REWARDED;
-      }
-      __syncwarp();
-      if (nr == P.Gr) {
-        if (P.red)
-          for (int m = 0; m < P.G; ++m) abort_member(P, D, C, cl, g * P.G + m);
-        if (P.filt && D.gfilt[C.grp_off + g]) filter_group(P, D, C, SS, g, cu, cl, m_reloc, err);
-        else complete_group(P, D, C, SS, g, cu, m_reloc, m_occ, err);
-        if (err) break;
-      }
-    }
-    for (int e = np + (int)lane; e < n; e += 32) D.ev_id[C.ev_off + e - np] = tmp[e];
+    np += __popc(okm);
+    if (err || okm != __ballot_sync(0xffffffffu, valid)) break;   // sorted: the rest are later
   }
+  __syncwarp();
+  // the events not yet due are carried to the next window, in order
+  for (int k = np + (int)lane; k < n; k += 32) D.ev_id[C.ev_off + k - np] = ev_id(k);
   __syncwarp();
   // Deadlock watchdog (the oracle's rule, DESIGN.md §4 R-WATCHDOG): no progress in this
   // window (cumulative progress metrics unchanged), nothing pending at its end, groups unconsumed

@@ -36,9 +36,12 @@ def combo_name(r: int, s: int, m: int) -> str:
     return "".join(("R" if r else "r", "S" if s else "s", "M" if m else "m"))
 
 
-def skewed_preset(n_seeds: int, eta: int = 3, instances: int = 4, steps: int = 6, sigma: float = 1.0) -> W.Preset:
+def skewed_preset(n_seeds: int, eta: int = 3, instances: int = 4, steps: int = 6, sigma: float = 1.0,
+                  kprefill_ps: int = 10_000_000, pull_lat_ps: int = 2 * W.PS_PER_S, train_windows: int = 5) -> W.Preset:
     """A §6.5-shaped workload scaled down (B=128, G=16, 40K, eta=3 on 128 GPUs): long-tailed
-    group-correlated lengths, every R/S/M combination for every seed."""
+    group-correlated lengths, every R/S/M combination for every seed.  kprefill_ps is the
+    prefill stall per re-admitted context token (reading A20) -- the KV recomputation an Interrupt
+    costs -- and pull_lat_ps the Pull duration q."""
     sc = []
     for seed in range(n_seeds):
         for (r, s, m) in COMBOS:
@@ -48,17 +51,17 @@ def skewed_preset(n_seeds: int, eta: int = 3, instances: int = 4, steps: int = 6
     return W.Preset("ablation", sc, 32, 8, W.LengthDist("uniform", 64, 1024),
                     W.LengthDist("lognormal", median=1024, sigma_g=sigma / np.sqrt(2), sigma_m=sigma / np.sqrt(2),
                                  cap=16_384),
-                    65_536, 5, steps)
+                    65_536, train_windows, steps, kprefill_ps=kprefill_ps, pull_lat_ps=pull_lat_ps)
+
+
+def scenario_inputs(p: W.Preset, k: int, ng: int):
+    """(prompt, target) of scenario k: seeds, not scenario indices, decide the lengths so that all 8
+    combos of a seed share inputs."""
+    return W.draw_lengths(dataclasses.replace(p, scenarios=[p.scenarios[k]]), 0, ng)
 
 
 def _draw_all(p: W.Preset, ng: int):
-    # seeds, not scenario indices, decide the lengths so that all 8 combos of a seed share inputs
-    prs, tgs = [], []
-    for k, sc in enumerate(p.scenarios):
-        base = dataclasses.replace(p, scenarios=[sc])
-        pr, tg = W.draw_lengths(base, 0, ng)
-        prs.append(pr)
-        tgs.append(tg)
+    prs, tgs = zip(*[scenario_inputs(p, k, ng) for k in range(len(p.scenarios))])
     return np.concatenate(prs), np.concatenate(tgs)
 
 
@@ -79,9 +82,10 @@ def run_to_steps(ctx, n_scen: int, steps: int, max_windows: int):
 
 
 def ablation(n_seeds: int = 16, steps: int = 6, eta: int = 3, instances: int = 4, max_windows: int = 6000,
-             sigma: float = 1.0) -> Dict:
+             sigma: float = 1.0, kprefill_ps: int = 10_000_000, pull_lat_ps: int = 2 * W.PS_PER_S,
+             train_windows: int = 5) -> Dict:
     from .staleflow import StaleFlow
-    p = skewed_preset(n_seeds, eta, instances, steps, sigma)
+    p = skewed_preset(n_seeds, eta, instances, steps, sigma, kprefill_ps, pull_lat_ps, train_windows)
     n = len(p.scenarios)
     ctx = StaleFlow.from_preset(p)
     pr, tg = _draw_all(p, p.pool_groups)
@@ -95,8 +99,15 @@ def ablation(n_seeds: int = 16, steps: int = 6, eta: int = 3, instances: int = 4
         rel = per[:, c] / base
         rows.append({"combo": combo_name(r, s, m), "tokens_per_s": float(np.nanmean(per[:, c])),
                      "vs_all_vanilla": float(np.nanmean(rel)), "seeds_done": int(np.isfinite(per[:, c]).sum())})
+    m = ctx.all_metrics()
+    ints = m[:, 6].reshape(n_seeds, len(COMBOS)).mean(0)
+    pulls = m[:, 7].reshape(n_seeds, len(COMBOS)).mean(0)
+    for c, row in enumerate(rows):
+        row["interrupts_per_seed"] = float(ints[c])
+        row["pulls_per_seed"] = float(pulls[c])
     return {"workload": {"instances": instances, "eta": eta, "B": p.batch_size, "G": p.group_size,
-                         "sigma": sigma, "steps": steps, "seeds": n_seeds}, "rows": rows}
+                         "sigma": sigma, "steps": steps, "seeds": n_seeds, "kprefill_ps": kprefill_ps,
+                         "pull_lat_ps": pull_lat_ps, "train_windows": train_windows}, "rows": rows}
 
 
 def staleness_by_buffer(ctx, scen: int, B: int) -> List[List[int]]:
@@ -147,10 +158,11 @@ def timeline(windows: int = 600, preset: str = "C3") -> Dict:
 
 
 def _print_ablation(res: Dict):
-    print("| combo (upper = StaleFlow) | tokens/s (simulated) | vs all-vanilla | seeds |")
-    print("|---|---|---|---|")
+    print("| combo (upper = StaleFlow) | tokens/s (simulated) | vs all-vanilla | seeds | interrupts | pulls |")
+    print("|---|---|---|---|---|---|")
     for r in res["rows"]:
-        print(f"| {r['combo']} | {r['tokens_per_s']:.0f} | {r['vs_all_vanilla']:.3f} | {r['seeds_done']} |")
+        print(f"| {r['combo']} | {r['tokens_per_s']:.0f} | {r['vs_all_vanilla']:.3f} | {r['seeds_done']} | "
+              f"{r['interrupts_per_seed']:.0f} | {r['pulls_per_seed']:.0f} |")
 
 
 def main(argv=None):
@@ -162,10 +174,14 @@ def main(argv=None):
     ap.add_argument("--instances", type=int, default=4)
     ap.add_argument("--sigma", type=float, default=1.0)
     ap.add_argument("--windows", type=int, default=600)
+    ap.add_argument("--kprefill", type=int, default=10_000_000, help="ps per re-admitted context token (A20)")
+    ap.add_argument("--pull", type=int, default=2 * W.PS_PER_S, help="Pull duration q (ps)")
+    ap.add_argument("--train-windows", type=int, default=5)
     ap.add_argument("--out", default=None)
     a = ap.parse_args(argv)
     if a.which == "ablation":
-        res = ablation(a.seeds, a.steps, a.eta, a.instances, sigma=a.sigma)
+        res = ablation(a.seeds, a.steps, a.eta, a.instances, sigma=a.sigma, kprefill_ps=a.kprefill,
+                       pull_lat_ps=a.pull, train_windows=a.train_windows)
         _print_ablation(res)
     elif a.which == "staleness":
         res = staleness(a.eta, windows=a.windows)

@@ -1,0 +1,39 @@
+"""The simulated experiments (paper_2601_12784_b200/experiments.py) run on the
+library; here a sampled ablation grid (fig:ablation: 2 seeds x the 8 R/S/M mixes) is
+recomputed by the oracle window by window and every scenario's metric vector, its time-to-K-steps
+and its tokens-at-K-steps (the experiment's throughput inputs) must match exactly."""
+import numpy as np
+import pytest
+
+from oracle.oracle import OracleSim
+from paper_2601_12784_b200 import experiments as E
+
+pytestmark = pytest.mark.gpu
+
+
+def test_ablation_grid_matches_oracle():
+    from paper_2601_12784_b200.staleflow import StaleFlow
+    steps = 3
+    p = E.skewed_preset(2, steps=steps)
+    n = len(p.scenarios)
+    g = StaleFlow.from_preset(p)
+    pr, tg = E._draw_all(p, p.pool_groups)
+    assert g.submit_many(np.arange(n), np.full(n, p.pool_groups), pr, tg) == 0
+    t_done, tok = E.run_to_steps(g, n, steps, 4000)
+    assert (t_done > 0).all()
+    windows = int(g.metrics()[0]) // n
+    o = OracleSim.from_preset(p)
+    for k in range(n):
+        assert o.submit(k, *E.scenario_inputs(p, k, p.pool_groups)) == 0
+    ot = np.full(n, -1, np.int64)
+    otok = np.zeros(n, np.int64)
+    for w in range(windows):
+        assert o.step(1, 8) == 0
+        m = np.stack([o.metrics(k) for k in range(n)])
+        hit = (m[:, 9] >= steps) & (ot < 0)
+        ot[hit] = m[hit, 26]
+        otok[hit] = m[hit, 3]
+    assert (ot == t_done).all() and (otok == tok).all()
+    gm = g.all_metrics()
+    for k in range(n):
+        assert (o.metrics(k) == gm[k]).all(), f"scenario {k} ({E.combo_name(*E.COMBOS[k % 8])})"

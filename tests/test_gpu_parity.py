@@ -155,3 +155,23 @@ def test_preemption_stress(seed, launch_mode):
     assert o.submit(0, prompt, target) == 0 and g.submit(0, prompt, target) == 0
     run_lockstep(o, g, [0], 150, every=3)
     assert o.metrics()[8] > 0                  # preemptions happened
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_reward_bursts_beyond_staging(seed, launch_mode):
+    """Reward bursts of 300-2048 events per window (mu = 0 routes the whole TS at once; k1 = 0 makes
+    steps short, so a batch completes inside one window): the ledger's shared-memory bitonic sort
+    (<= 512 events) and its global-scratch sort (more) must apply rewards in exactly the oracle's
+    (t_reward, id) order (W8, P:366, 378-382)."""
+    rng = random.Random(4000 + seed)
+    B, G, I, eta = 128, 8, 8, 1
+    cfg = Config(batch_size=B, n_scenarios=1, k1=0, k2=100, k3=1, k4=50, k5=1, kp=0, M=1 << 20, mu=0.0,
+                 phi_tp=50.0, phi_wait=1000, delta=6000, r=5, q=300, R=6000, strategy=rng.choice([7, 5]), atw=1,
+                 pool_capacity_groups=B * 8)
+    prompt = np.array([rng.randint(1, 20) for _ in range(B * 8)], np.int32)
+    target = np.array([rng.randint(30, 40) for _ in range(B * 8 * G)], np.int32)
+    o = OracleSim(I, eta, G, cfg)
+    g = gpu_from_config(I, eta, G, cfg)
+    assert o.submit(0, prompt, target) == 0 and g.submit(0, prompt, target) == 0
+    run_lockstep(o, g, [0], 24, every=1)
+    assert o.metrics()[9] >= 6                   # batches
