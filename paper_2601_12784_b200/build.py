@@ -17,6 +17,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # L1-cached load could return a line filled with pre-release data by another warp of the SM
 # (measured: an SF_CHECK build diverged under PDL, bit-exact with L1 bypassed).
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-dlcm=cg", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"]
+if os.environ.get("SF_L1_LOADS") == "1":          # experiment only: L1-cached global loads
+    FLAGS = [f for f in FLAGS if f not in ("-Xptxas", "-dlcm=cg")]
 FLAGS += [f for f in os.environ.get("SF_NVCC_EXTRA", "").split() if f]
 
 

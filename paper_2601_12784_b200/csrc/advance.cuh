@@ -70,8 +70,10 @@ __device__ __forceinline__ int compact_wait_aborted(const Dev &D, const ScenCons
 }
 
 // ------------------------------------------------------------------ register-resident path
-// Dead / empty slots hold a sentinel remaining length (kDead) so a decode step is a plain
-// decrement + ballot per register row with no live-mask test; a window has far fewer than kDead
+// Each live slot holds dn = the window's decode-step count at whose end it completes (its remaining
+// length is dn - tc, tc = steps ended so far in the window; run_done - itick in HBM), so a decode
+// step touches no slot: it completes the slots with dn == tc, and only when tc reaches the
+// warp-uniform minimum mind.  Dead / empty slots hold a sentinel (kDead); a window has far fewer than kDead
 // steps.  Every live slot also keeps its trajectory's target T and final context p + T in
 // registers, so completions and preemptions need no memory loads; completion events are
 // buffered in shared memory and reserved in the scenario's event list with one atomic per
@@ -95,20 +97,57 @@ __device__ __forceinline__ void flush_events(const Dev &D, long long lb, InstSta
   n = 0;
 }
 
+// An instance's run list and step count as loaded before its coordinator has finished: only the
+// advance writes them, so once the scenario's previous window is complete (f_led) they are final,
+// and a warp can load them while its coordinator still runs (k_advance, PDL).
+struct RunPre {
+  int run_n, itick;
+  int dn[kR], id[kR], T[kR], fin[kR];
+};
+
+__device__ __forceinline__ void preload_run(const Dev &D, const ScenConst &C, int gi, RunPre &r) {
+  const int lane = (int)lane_id();
+  const long long lb = C.list_off + (long long)(gi - C.inst_off) * C.cap;
+  r.run_n = D.irun_n[gi];
+  r.itick = D.itick[gi];
+#pragma unroll
+  for (int q = 0; q < kR; ++q) {
+    const int s = q * 32 + lane;
+    r.dn[q] = kDead; r.id[q] = 0; r.T[q] = 0; r.fin[q] = 0;
+    if (s < r.run_n) {
+      r.dn[q] = D.run_done[lb + s] - r.itick; r.id[q] = D.run_id[lb + s]; r.T[q] = D.run_T[lb + s];
+      r.fin[q] = D.run_fin[lb + s];
+    }
+  }
+}
+
 static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenConst &C, ScenState &SS, InstState &x,
-                                   long long lb, long long t_end, AdvStage &sm) {
+                                   long long lb, long long t_end, AdvStage &sm, const RunPre *pre) {
   const unsigned lane = lane_id();
   const int cap = C.cap;
   const long long k5 = P.k5;
-  int rem[kR], rid[kR], tq[kR], fin[kR];     // remaining, id, target T, final context p + T
+  int rem[kR], rid[kR], tq[kR], fin[kR];     // dn (completion step, see above), id, target T, final context p + T
   unsigned live[kR];
+  const int it0 = x.itick;
+  int tc = 0;                                // decode steps ended in this window
+  int n_orig = x.run_n;                      // slots [0, n_orig) mirror HBM until a compaction
 #pragma unroll
   for (int q = 0; q < kR; ++q) {
     const int s = q * 32 + (int)lane;
-    rem[q] = kDead; rid[q] = 0; tq[q] = 0; fin[q] = 0;
-    if (s < x.run_n) { rem[q] = D.run_done[lb + s] - x.itick; rid[q] = D.run_id[lb + s]; tq[q] = D.run_T[lb + s]; fin[q] = D.run_fin[lb + s]; }
+    if (pre) { rem[q] = pre->dn[q]; rid[q] = pre->id[q]; tq[q] = pre->T[q]; fin[q] = pre->fin[q]; }
+    else {
+      rem[q] = kDead; rid[q] = 0; tq[q] = 0; fin[q] = 0;
+      if (s < x.run_n) { rem[q] = D.run_done[lb + s] - it0; rid[q] = D.run_id[lb + s]; tq[q] = D.run_T[lb + s]; fin[q] = D.run_fin[lb + s]; }
+    }
     live[q] = __ballot_sync(0xffffffffu, s < x.run_n);
   }
+  auto min_dn = [&]() {                      // earliest completion step among the live slots
+    int m = kDead;
+#pragma unroll
+    for (int q = 0; q < kR; ++q) m = min(m, rem[q]);
+    return warp_min(m);
+  };
+  int mind = min_dn();
   // Arrivals are read through two 32-wide register windows, each refilled with one coalesced
   // load per 32 arrivals: window 6 (id, t_arr) for delivery in B6, window 7 (id, gen, T, prompt)
   // for admission in B7.  Lane k of a window holds arrival base + k.
@@ -130,7 +169,7 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
       a7_gen = D.gen[j]; a7_T = D.T[j]; a7_p = D.prompt[C.grp_off + grp_of(P, a7_id)];
     }
   };
-  if (x.arr_n > 0) { load6(0); load7(0); }
+  if (x.arr_n > 0) { load6(0); load7(0); }      // (load6(0) is also issued speculatively in advance_instance)
   int arr_ring0 = -1;                       // wait-ring position of arrival 0 once appended
   int nlive = x.run_n, tail = x.run_n, n_ev = 0;
   // arrival k's time (k only grows): window 6, refilled when k leaves it
@@ -160,7 +199,7 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
       if (x.intkind == INT_ALL) {
 #pragma unroll
         for (int q = 0; q < kR; ++q) { live[q] = 0u; rem[q] = kDead; }
-        nlive = 0; tail = 0; x.wn = 0; x.kv = 0;
+        nlive = 0; tail = 0; x.wn = 0; x.kv = 0; mind = kDead;
       } else {
         x.wn -= x.intk;                                  // wait tail (A7)
       }
@@ -177,8 +216,8 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
         const bool a = ((live[q] >> lane) & 1u) && D.loc[C.traj_off + rid[q]] == L_ABORTED;
         const unsigned am = __ballot_sync(0xffffffffu, a);
         if (a) {
-          release += k5 * (long long)(fin[q] - rem[q]);                           // p + gen
-          D.gen[C.traj_off + rid[q]] = tq[q] - rem[q];                           // progress kept
+          release += k5 * (long long)(fin[q] - (rem[q] - tc));                    // p + gen
+          D.gen[C.traj_off + rid[q]] = tq[q] - (rem[q] - tc);                    // progress kept
           rem[q] = kDead;
         }
         live[q] &= ~am;
@@ -187,6 +226,7 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
       if (nab) {
         x.kv -= warp_sum(release);
         nlive -= nab;
+        mind = min_dn();
         int t = 0;
 #pragma unroll
         for (int q = 0; q < kR; ++q)
@@ -203,13 +243,14 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
       // B2 + B3 in registers: one token per running trajectory, ballot the completions
       const int n0 = nlive;
       unsigned d[kR], dany = 0;
+      ++tc;
+      if (tc == mind) {
 #pragma unroll
-      for (int q = 0; q < kR; ++q) {
-        rem[q] -= 1;
-        d[q] = __ballot_sync(0xffffffffu, rem[q] == 0);
-        dany |= d[q];
+        for (int q = 0; q < kR; ++q) {
+          d[q] = __ballot_sync(0xffffffffu, rem[q] == tc);
+          dany |= d[q];
+        }
       }
-      x.itick += 1;
       x.kv += k5 * n0;
       x.tokens += n0;
       if (dany) {
@@ -245,6 +286,7 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
           if (live[q]) t = q * 32 + 32 - __clz(live[q]);
         tail = t;
         blocked = false;
+        mind = min_dn();
         __syncwarp();
       }
       x.st = I_IDLE;
@@ -264,7 +306,8 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
         for (int q = 0; q < kR; ++q)
           if (q == hq) { hm = live[q]; r_ = rem[q]; i_ = rid[q]; t_ = tq[q]; f_ = fin[q]; }
         const int hl = 31 - __clz(hm);
-        const int r = __shfl_sync(0xffffffffu, r_, hl);
+        const int dv = __shfl_sync(0xffffffffu, r_, hl);
+        const int r = dv - tc;                         // remaining
         const int id = __shfl_sync(0xffffffffu, i_, hl);
         const int Tj = __shfl_sync(0xffffffffu, t_, hl);
         const int fj = __shfl_sync(0xffffffffu, f_, hl);
@@ -287,6 +330,7 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
           }
         --nlive;
         tail = hq * 32 + hl;
+        if (dv == mind) mind = min_dn();
         ++x.wn;
         ++x.preempts;
         head_ok = true; head_id = id; head_gen = g_; head_T = Tj; head_ctx = ctx;
@@ -370,18 +414,21 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
           }
           __syncwarp();
           tail = nlive;
+          n_orig = 0;
         }
         const int s = tail++;
         const int sq = s >> 5, sl = s & 31;
+        n_orig = min(n_orig, s);                       // a reused slot no longer mirrors HBM
 #pragma unroll
         for (int q = 0; q < kR; ++q)
           if (q == sq) {
             if ((int)lane == sl) {
-              rem[q] = head_T - head_gen; rid[q] = head_id;
+              rem[q] = tc + head_T - head_gen; rid[q] = head_id;
               tq[q] = head_T; fin[q] = (int)(head_ctx - head_gen) + head_T;
             }
             live[q] |= 1u << sl;
           }
+        mind = min(mind, tc + head_T - head_gen);
         if (lane == 0) D.loc[C.traj_off + head_id] = L_RUN;
         x.kv += k5 * head_ctx;
         x.prefill += head_ctx;
@@ -404,7 +451,7 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
       continue;
     }
     // Quiet decode steps: the next boundary is a step end with no pending command, no
-    // completion (no live rem == 1), no preemption (kv + k5 n <= M), no arrival due, and no
+    // completion (tc + 1 < mind), no preemption (kv + k5 n <= M), no arrival due, and no
     // admission possible (B7 just left the head blocked or the queue empty).  Such a boundary
     // only credits the step (B2) and starts the next one (B8).
     if (x.intkind == INT_NONE && !x.pullpend) {
@@ -417,10 +464,7 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
         // b_j < next arrival.  m = the largest such j: g is increasing, so x = m - 1 is the floor
         // root of g(x) = t_lim - nb, estimated in fp64 and then fixed by exact integer checks (int64
         // when the products provably fit, else int128).
-        int mr = kDead;
-#pragma unroll
-        for (int q = 0; q < kR; ++q) mr = min(mr, rem[q]);
-        mr = warp_min(mr);
+        const int mr = mind - tc;                               // the earliest remaining length
         long long m_hi = (long long)mr - 1;
         m_hi = min(m_hi, (long long)((unsigned)(P.M - x.kv) / (unsigned)k5n));   // M - kv < 2^30
         const long long t_lim = min(t_end, next_arr - 1);
@@ -465,9 +509,7 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
         }
 #endif
         if (m > 0) {
-#pragma unroll
-          for (int q = 0; q < kR; ++q) rem[q] -= (int)m;
-          x.itick += (int)m;
+          tc += (int)m;
           x.nb = (long long)((__int128)x.nb + gm);                   // b_{m+1} = nb + g(m)
           x.kv += m * k5n;
           x.tokens += m * nlive;
@@ -477,14 +519,8 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
       } else {
         for (;;) {
           const long long bq = x.nb;
-          if (bq > t_end || x.kv + k5n > P.M || next_arr <= bq) break;
-          unsigned one = 0;
-#pragma unroll
-          for (int q = 0; q < kR; ++q) one |= __ballot_sync(0xffffffffu, rem[q] == 1);
-          if (one) break;
-#pragma unroll
-          for (int q = 0; q < kR; ++q) rem[q] -= 1;
-          x.itick += 1;
+          if (bq > t_end || x.kv + k5n > P.M || next_arr <= bq || tc + 1 >= mind) break;
+          ++tc;
           x.kv += k5n;
           x.tokens += nlive;
           x.nb = bq + (long long)P.k1i * (int)x.kv + cn;
@@ -499,22 +535,26 @@ static __device__ void advance_reg(const GParams &P, const Dev &D, const ScenCon
   assert(x.evn <= C.cap);
   assert(nlive >= 0 && nlive <= 32 * kR && x.wn >= 0 && x.wn <= cap && x.kv >= 0 && x.kv <= P.M);
 #pragma unroll
-  for (int q = 0; q < kR; ++q) assert(!((live[q] >> lane) & 1u) || (rem[q] > 0 && rem[q] <= tq[q]));
+  for (int q = 0; q < kR; ++q) assert(!((live[q] >> lane) & 1u) || (rem[q] - tc > 0 && rem[q] - tc <= tq[q]));
 #endif
-  // write the run list back compacted, in admission order
+  // write the run list back compacted, in admission order; an entry that kept its slot since the
+  // window start is unchanged in HBM (run_done is absolute) and is not rewritten
   int before = 0;
 #pragma unroll
   for (int q = 0; q < kR; ++q) {
     if ((live[q] >> lane) & 1u) {
       const int pos = before + __popc(live[q] & lanemask_lt());
-      D.run_done[lb + pos] = rem[q] + x.itick;
-      D.run_id[lb + pos] = rid[q];
-      D.run_T[lb + pos] = tq[q];
-      D.run_fin[lb + pos] = fin[q];
+      if (pos != q * 32 + (int)lane || pos >= n_orig) {
+        D.run_done[lb + pos] = it0 + rem[q];                 // = itick after the window + remaining
+        D.run_id[lb + pos] = rid[q];
+        D.run_T[lb + pos] = tq[q];
+        D.run_fin[lb + pos] = fin[q];
+      }
     }
     before += __popc(live[q]);
   }
   x.run_n = nlive;
+  x.itick = it0 + tc;
 }
 
 // ------------------------------------------------------------------ global-memory path
@@ -680,7 +720,7 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
 // s = D.inst_scen[gi] and C = D.sc[s] are passed in so that a caller can load them (never written
 // by a window) before waiting on the coordinator's flag.
 __device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D, int gi, AdvStage &stage, int s,
-                                                 const ScenConst C) {
+                                                 const ScenConst C, const RunPre *pre = nullptr) {
   const unsigned lane = lane_id();
 #ifdef SF_TIMING
   const long long t0_adv = clock64();
@@ -691,10 +731,11 @@ __device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D,
   x.pullv = D.ipullv[gi]; x.pullpend = D.ipullpend[gi];
   x.intkind = D.iintkind[gi]; x.intk = D.iintk[gi];
   x.kv = D.ikv[gi]; x.prefill = D.iprefill[gi]; x.cc = D.ic[gi]; x.v = D.iv[gi];
-  x.run_n = D.irun_n[gi]; x.whead = D.iwhead[gi]; x.wn = D.iwn[gi];
+  x.whead = D.iwhead[gi]; x.wn = D.iwn[gi];
   x.arr_n = D.iarr_n[gi]; x.arr_head = 0;
   x.abortn = D.iabort[gi]; x.abortarr = D.iabort_arr[gi]; x.evn = D.iev_n[gi];
-  x.itick = D.itick[gi];
+  if (pre) { x.run_n = pre->run_n; x.itick = pre->itick; }
+  else { x.run_n = D.irun_n[gi]; x.itick = D.itick[gi]; }
   ScenState &SS = D.ss[s];
   const int err0 = SS.err;    // checked below, before the first write
   const int i = gi - C.inst_off;
@@ -706,7 +747,7 @@ __device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D,
   x.t_cmd = (x.st == I_IDLE && (x.pullpend || x.intkind != INT_NONE || x.abortn > 0)) ? t : kInf;
 
   if (err0) return;
-  if (x.run_n + x.wn + x.arr_n <= 32 * kR) advance_reg(P, D, C, SS, x, lb, t_end, stage);
+  if (x.run_n + x.wn + x.arr_n <= 32 * kR) advance_reg(P, D, C, SS, x, lb, t_end, stage, pre && pre->run_n <= 32 * kR ? pre : nullptr);
   else advance_global(P, D, C, SS, x, lb, t_end);
 
   // keep undelivered arrivals (held while pulling / later than the window) at the list front

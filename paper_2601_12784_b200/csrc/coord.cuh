@@ -35,6 +35,7 @@ struct Cyc {                   // lane-uniform per-cycle scalars
   long long t;
   int cu, ps, eta, I, G, B;
   int n_v, n_vl, vl_head, n_ingested, min_live_g;
+  int min_v;                   // smallest version in the versioned MLQ (its first item's)
   long long window;
   unsigned long long hash;
   int cmd_n;
@@ -438,6 +439,19 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
   int k = 0;
   bool stop = false;
   int knext = 0;
+  {
+    // the MLQ's first item has no candidate instance: stop before any prefetch.  It is
+    // the lowest-version versioned item (candidates: v_i >= min_v) or, without versioned items, the
+    // first member of a versionless group (candidates: verify(v_i), the bitmask vmask)
+    bool any = false;
+#pragma unroll
+    for (int q = 0; q < KS; ++q) {
+      const int i = (int)lane + 32 * q;
+      any |= i < c.I && (c.n_v > 0 ? S.v[q] >= c.min_v
+                                   : (S.v[q] >= vbase && ((vmask >> (S.v[q] - vbase)) & 1u)));
+    }
+    if (total > 0 && !__any_sync(0xffffffffu, any)) { stop = true; knext = total; }
+  }
 #ifdef SF_TIMING_ROUTE
   c.rt_last = clock64();
 #endif
@@ -1003,6 +1017,7 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
     int min_v = 0x7fffffff;
     c.n_v = build_mlq(P, D, C, c, sg, &min_v);
     if (min_v < 0) c.mlq_err = 1;
+    c.min_v = min_v;
     c.n_vl = (c.n_ingested - c.vl_head) * c.G;
 
     SF_CK(0);
@@ -1141,9 +1156,13 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
     }
     SF_CK(2);
     // ---------------- W5: routing (Alg 2) over the TS incl. interrupted trajectories
-    c.n_v = build_mlq(P, D, C, c, sg, &min_v);
+    // (the versioned MLQ changes only if W3/W4 interrupted something: otherwise the first build stands)
+    if (m_interrupts > 0) {
+      c.n_v = build_mlq(P, D, C, c, sg, &min_v);
+      if (min_v < 0) c.mlq_err = 1;
+      c.min_v = min_v;
+    }
     SF_CK(3);
-    if (min_v < 0) c.mlq_err = 1;
 #ifdef SF_TIMING
     const long long t_rp = clock64();
 #endif

@@ -14,9 +14,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, SF_ADV_MINB) k_advance(GP
   if (gi >= n_inst_total) return;
   const int s = D.inst_scen[gi];
   const ScenConst C = D.sc[s];                     // constant: its load overlaps the wait
+  // the scenario's previous window is complete: this instance's run list is final -- load it while
+  // the coordinator runs, then wait for the coordinator
+  if (P.pdl) warp_wait_geq(&D.f_led[s], P.epoch - 1);
+  RunPre pre;
+  preload_run(D, C, gi, pre);
   if (P.pdl) warp_wait_geq(&D.f_coord[s], P.epoch);     // this scenario's coordinator is done
   SF_TRACE_AT(4LL * P.n_scen + 2LL * gi);
-  advance_instance(P, D, gi, stage_all[threadIdx.x >> 5], s, C);
+  advance_instance(P, D, gi, stage_all[threadIdx.x >> 5], s, C, &pre);
   SF_TRACE_AT(4LL * P.n_scen + 2LL * gi + 1);
   __threadfence();                                 // this lane's writes, device-wide
   __syncwarp();

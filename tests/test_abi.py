@@ -87,3 +87,27 @@ def test_group_division_multiply_shift_exact():
         ids = list(range(5000)) + [rng.randrange(top) for _ in range(5000)] + [top - 1 - k for k in range(500)]
         assert all((i * m) < (1 << 64) and ((i * m) & ((1 << 64) - 1)) >> 40 == i // G for i in ids), G
     assert (((1 << 24) * (1 << 40)) & ((1 << 64) - 1)) >> 40 == 0   # the wrap sf_create now rejects (G = 1)
+
+
+def test_window_kernels_use_strong_gpu_loads_only():
+    """The window kernels hand data over per scenario through release/acquire flags while other
+    scenarios' kernels run on the same SMs (programmatic dependent launch).  The
+    library is built so that every global load is a .STRONG.GPU load served by L2 (-dlcm=cg); a
+    build without it (weak, L1-cached LDG.E) fails here rather than running with L1 lines that may
+    hold pre-release data."""
+    import shutil
+    import subprocess
+    from paper_2601_12784_b200 import build as B
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(cuobjdump):
+        pytest.skip("cuobjdump not available")
+    B.build()
+    sass = subprocess.run([cuobjdump, "-sass", B.LIB], capture_output=True, text=True, check=True).stdout
+    weak, func = {}, None
+    for line in sass.splitlines():
+        if "Function :" in line:
+            func = line.split("Function :")[1].strip()
+        elif func and "LDG." in line and ".STRONG.GPU" not in line:
+            weak[func] = weak.get(func, 0) + 1
+    window = [f for f in weak if any(k in f for k in ("k_begin_coord", "k_advance", "k_ledger", "k_window"))]
+    assert not window, f"weak (L1-cached) global loads in window kernels: {[(f, weak[f]) for f in window]}"
