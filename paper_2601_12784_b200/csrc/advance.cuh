@@ -19,7 +19,10 @@ namespace sf {
 
 constexpr long long kInf = 0x7fffffffffffffffLL;
 constexpr int kR = 4;                      // register rows -> 128 run slots per instance
-constexpr int kWarpsPerBlock = 8;
+#ifndef SF_ADV_WARPS
+#define SF_ADV_WARPS 8
+#endif
+constexpr int kWarpsPerBlock = SF_ADV_WARPS;
 
 struct InstState {
   int st, pullv, pullpend, intkind, intk, cc, v, run_n, whead, wn, arr_n, arr_head;

@@ -5,7 +5,7 @@
 namespace sf {
 
 #ifndef SF_ADV_MINB
-#define SF_ADV_MINB 2      // measured best: 2 blocks x 8 warps per SM (128 registers, no spills)
+#define SF_ADV_MINB (16 / SF_ADV_WARPS)   // 16 warps per SM (128 registers, no spills)
 #endif
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, SF_ADV_MINB) k_advance(GParams P, Dev D, int n_inst_total) {
   __shared__ AdvStage stage_all[kWarpsPerBlock];

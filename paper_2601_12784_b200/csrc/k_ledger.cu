@@ -4,7 +4,7 @@
 
 namespace sf {
 
-__global__ void __launch_bounds__(128) k_ledger(GParams P, Dev D) {
+__global__ void __launch_bounds__(32 * kLedgerWarps) k_ledger(GParams P, Dev D) {
   __shared__ EvStage stage_all[kLedgerWarps];
   pdl_trigger();                                   // the next window's coordinator may be scheduled
   const int s = blockIdx.x * kLedgerWarps + (threadIdx.x >> 5);
@@ -183,7 +183,7 @@ __global__ void k_commit_pool(Dev D, const int *desc, int n_desc) {
 }  // namespace sf
 
 void sf_launch_ledger(const sf::GParams &P, const sf::Dev &D, int n_scen, cudaStream_t st) {
-  sf_launch_pdl(sf::k_ledger, (n_scen + sf::kLedgerWarps - 1) / sf::kLedgerWarps, 128, st, P.pdl, P, D);
+  sf_launch_pdl(sf::k_ledger, (n_scen + sf::kLedgerWarps - 1) / sf::kLedgerWarps, 32 * sf::kLedgerWarps, st, P.pdl, P, D);
 }
 void sf_launch_collect(const sf::GParams &P, const sf::Dev &D, int scen, int *out_dev, cudaStream_t st) {
   sf::k_collect<<<1, 32, 0, st>>>(P, D, scen, out_dev);

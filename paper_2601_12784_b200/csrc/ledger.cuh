@@ -12,7 +12,10 @@
 
 namespace sf {
 
-constexpr int kLedgerWarps = 4;
+#ifndef SF_LEDGER_WARPS
+#define SF_LEDGER_WARPS 4
+#endif
+constexpr int kLedgerWarps = SF_LEDGER_WARPS;
 
 __device__ __forceinline__ long long ring_base(const ScenConst &C, int B, int b) {
   return C.led_off + (long long)(b % (C.eta + 1)) * B;

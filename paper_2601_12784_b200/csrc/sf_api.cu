@@ -27,6 +27,7 @@ struct sf_ctx {
   int n_inst_total = 0;
   int max_inst = 1;
   int fused = 0;                      // launch mode: 1 = one fused window kernel (k_window)
+  int block = 0;                      // launch mode: one block per scenario for the whole call (k_window_block)
   int pdl = 1;                        // programmatic dependent launch between window kernels
   int lanes = 0;                      // split mode: one-lane-per-instance advance kernel (SF_ADVANCE=lanes)
   int pdl_mask = 0;                   // debugging (SF_PDL_MASK): bit 0 serializes the advance, bit 1 the ledger
@@ -260,10 +261,19 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
     c->P.skip = strcmp(m, "step") != 0;
     c->lanes = strcmp(m, "lanes") == 0;
   }
+  // few scenarios (at most one per SM): one block per scenario for the whole call (k_window_block,
+  // the window's phases separated by __syncthreads instead of kernel launches); many scenarios: the
+  // three-kernel split with programmatic dependent launch (measured)
+  {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device);
+    c->block = ns <= sms;
+  }
   if (const char *m = getenv("SF_LAUNCH")) {
-    if (!strcmp(m, "split")) { c->fused = 0; c->dyn = 0; }
-    if (!strcmp(m, "fused")) { c->fused = c->max_inst <= 32; c->dyn = 0; }
-    if (!strcmp(m, "dyn")) { c->fused = 0; c->dyn = 1; }
+    if (!strcmp(m, "split")) { c->fused = 0; c->dyn = 0; c->block = 0; }
+    if (!strcmp(m, "fused")) { c->fused = c->max_inst <= 32; c->dyn = 0; c->block = 0; }
+    if (!strcmp(m, "dyn")) { c->fused = 0; c->dyn = 1; c->block = 0; }
+    if (!strcmp(m, "block")) { c->fused = 0; c->dyn = 0; c->block = 1; }
   }
   const long long ntraj = (long long)ns * pool_traj, ngrp = (long long)ns * P.pool_cap;
   Dev &D = c->D;
@@ -445,12 +455,18 @@ sf_status sf_step(sf_ctx *c, int32_t n_windows, sf_step_stats *out) {
     prof_mark(c, 3);
     c->launches += 1;
   }
+  if (c->block && !c->fused && n_windows > 0) {
+    prof_mark(c, 3);
+    sf_launch_window_block(c->P, c->D, c->n_scen, c->max_inst, n_windows, c->stream);
+    prof_mark(c, 3);
+    c->launches += 1;
+  }
   // Split mode: three kernels per window.  With PDL each kernel may start while its predecessor
   // runs and waits per scenario on the progress flags (epoch = split windows so far), so a
   // scenario's advance starts when ITS coordinator is done instead of after the slowest one.
   // Profiling (events between kernels) serializes the launches.
   const int pdl = c->pdl && !c->prof_on;
-  const bool dyn = c->dyn && !c->fused && !c->prof_on;   // profiling attributes time per kernel: split
+  const bool dyn = c->dyn && !c->fused && !c->block && !c->prof_on;   // profiling attributes time per kernel: split
   if (dyn && n_windows > 0) {
     if (c->dyn_blocks == 0) c->dyn_blocks = sf_dyn_blocks(c->max_inst);
     const size_t qbytes = sizeof(int) * (4 + (size_t)c->n_scen + (size_t)c->D.q_total);
@@ -463,7 +479,7 @@ sf_status sf_step(sf_ctx *c, int32_t n_windows, sf_step_stats *out) {
       c->launches += 1;
     }
   }
-  for (int w = 0; w < (c->fused || dyn ? 0 : n_windows); ++w) {
+  for (int w = 0; w < (c->fused || c->block || dyn ? 0 : n_windows); ++w) {
     GParams P = c->P;
     P.epoch = ++c->epoch;
     P.pdl = pdl && w > 0;                 // the first coordinator follows arbitrary stream work

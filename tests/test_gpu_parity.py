@@ -1,7 +1,7 @@
 """GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
 
 Bar: bit-exact on every integer observable (DESIGN.md §2 makes the fp64 cost-model decisions
-identical too): per-scenario metric vectors (incl. the FNV command hash), the full command log,
+identical too): per-scenario metric vectors (incl. the order-sensitive command checksum), the full command log,
 every trajectory's lifecycle record, every batch composition and every instance's state.
 """
 import random
@@ -16,12 +16,14 @@ from tests.parity import compare, make_pair, run_lockstep, submit_both
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["auto", "lanes", "fused", "step", "dyn", "nopdl"])
+@pytest.fixture(params=["auto", "split", "lanes", "fused", "block", "step", "dyn", "nopdl"])
 def launch_mode(request, monkeypatch):
-    """Every launch / decode-step mode must give identical results: default (three kernels with
-    programmatic dependent launch, one warp per instance and closed-form quiet steps in the
-    advance), the one-lane-per-instance advance, fused window kernel, one-by-one decode steps, the
-    dataflow window kernel, and three fully serialized kernels."""
+    """Every launch / decode-step mode must give identical results: the default (a block per
+    scenario for contexts with at most one scenario per SM, else the split), the split (three
+    kernels with programmatic dependent launch, one warp per instance and closed-form quiet steps
+    in the advance), the one-lane-per-instance advance, the fused window kernel, the
+    block-per-scenario window kernel, one-by-one decode steps, the dataflow window kernel, and three
+    fully serialized kernels."""
     monkeypatch.delenv("SF_LAUNCH", raising=False)
     monkeypatch.delenv("SF_ADVANCE", raising=False)
     monkeypatch.delenv("SF_PDL", raising=False)
@@ -31,6 +33,10 @@ def launch_mode(request, monkeypatch):
         monkeypatch.setenv("SF_PDL", "0")
     if request.param == "fused":
         monkeypatch.setenv("SF_LAUNCH", "fused")
+    if request.param == "block":
+        monkeypatch.setenv("SF_LAUNCH", "block")
+    if request.param in ("split", "lanes", "step", "nopdl"):
+        monkeypatch.setenv("SF_LAUNCH", "split")
     if request.param == "step":
         monkeypatch.setenv("SF_ADVANCE", "step")
     if request.param == "lanes":
