@@ -722,14 +722,9 @@ static __device__ void advance_global(const GParams &P, const Dev &D, const Scen
 // One window of W6-W7 for global instance gi, executed by one warp (stage: 32*kR int2 of smem).
 // s = D.inst_scen[gi] and C = D.sc[s] are passed in so that a caller can load them (never written
 // by a window) before waiting on the coordinator's flag.
-__device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D, int gi, AdvStage &stage, int s,
-                                                 const ScenConst C, const RunPre *pre = nullptr) {
-  const unsigned lane = lane_id();
-#ifdef SF_TIMING
-  const long long t0_adv = clock64();
-#endif
-  // the instance's own fields depend only on gi: issue them with the scenario lookups, not after
-  InstState x;
+// The instance's window-start fields (written by the previous window's advance and by this
+// window's coordinator): valid once the coordinator of this window is done.
+__device__ __forceinline__ void load_inst_state(const Dev &D, int gi, InstState &x) {
   x.st = D.ist[gi]; x.nb = D.inb[gi]; x.until = D.iuntil[gi];
   x.pullv = D.ipullv[gi]; x.pullpend = D.ipullpend[gi];
   x.intkind = D.iintkind[gi]; x.intk = D.iintk[gi];
@@ -737,6 +732,21 @@ __device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D,
   x.whead = D.iwhead[gi]; x.wn = D.iwn[gi];
   x.arr_n = D.iarr_n[gi]; x.arr_head = 0;
   x.abortn = D.iabort[gi]; x.abortarr = D.iabort_arr[gi]; x.evn = D.iev_n[gi];
+}
+
+// xs: the fields already loaded by load_inst_state (a caller that prefetches them while the
+// warp's previous instance is processed), else loaded here.
+__device__ __forceinline__ void advance_instance(const GParams &P, const Dev &D, int gi, AdvStage &stage, int s,
+                                                 const ScenConst C, const RunPre *pre = nullptr,
+                                                 const InstState *xs = nullptr) {
+  const unsigned lane = lane_id();
+#ifdef SF_TIMING
+  const long long t0_adv = clock64();
+#endif
+  // the instance's own fields depend only on gi: issue them with the scenario lookups, not after
+  InstState x;
+  if (xs) x = *xs;
+  else load_inst_state(D, gi, x);
   if (pre) { x.run_n = pre->run_n; x.itick = pre->itick; }
   else { x.run_n = D.irun_n[gi]; x.itick = D.itick[gi]; }
   ScenState &SS = D.ss[s];

@@ -112,18 +112,44 @@ static __device__ int build_mlq(const GParams &P, const Dev &D, const ScenConst 
   int *tmp = D.mlq + C.mlq_off + C.cap;
   int *out = D.mlq + C.mlq_off;
   int n_tmp = 0;
-  for (int w0 = w_lo; w0 < w_hi; w0 += 32) {
-    unsigned word = (w0 + (int)lane < w_hi) ? D.tsv_bits[C.bits_off + w0 + lane] : 0u;
-    const int cnt = __popc(word);
-    const int off = warp_excl_scan(cnt);
-    const int tot = __shfl_sync(0xffffffffu, off + cnt, 31);
-    int pos = n_tmp + off;
-    while (word) {
-      const int b = __ffs(word) - 1;
-      word &= word - 1;
-      tmp[pos++] = ((w0 + (int)lane) << 5) + b;
+  // only the chunks of 32 words whose summary bit is set (D.tsv_sum), in ascending order; a chunk
+  // found all-zero has its summary bit cleared (bits are set only by tsv_mark)
+  if (w_lo < w_hi) {
+    const int c_lo = w_lo >> 5, c_hi = (w_hi - 1) >> 5;          // chunks [c_lo, c_hi]
+    for (int s0 = c_lo >> 5; s0 <= (c_hi >> 5); s0 += 32) {
+      const int sw = s0 + (int)lane;
+      unsigned sm = sw <= (c_hi >> 5) ? D.tsv_sum[C.sum_off + sw] : 0u;
+      if (sw == (c_lo >> 5)) sm &= ~0u << (c_lo & 31);
+      if (sw == (c_hi >> 5) && (c_hi & 31) != 31) sm &= (2u << (c_hi & 31)) - 1u;
+      unsigned lanes = __ballot_sync(0xffffffffu, sm != 0u);
+      while (lanes) {
+        const int L = __ffs(lanes) - 1;
+        lanes &= lanes - 1;
+        unsigned bits = __shfl_sync(0xffffffffu, sm, L);
+        while (bits) {
+          const int b = __ffs(bits) - 1;
+          bits &= bits - 1;
+          const int ch = ((s0 + L) << 5) + b;
+          const int w = (ch << 5) + (int)lane;
+          const unsigned raw = D.tsv_bits[C.bits_off + w];     // the chunk lies inside the scenario's words
+          unsigned word = (w >= w_lo && w < w_hi) ? raw : 0u;
+          if (!__any_sync(0xffffffffu, raw != 0u)) {
+            if (lane == 0) atomicAnd(&D.tsv_sum[C.sum_off + (ch >> 5)], ~(1u << (ch & 31)));
+            continue;
+          }
+          const int cnt = __popc(word);
+          const int off = warp_excl_scan(cnt);
+          const int tot = __shfl_sync(0xffffffffu, off + cnt, 31);
+          int pos = n_tmp + off;
+          while (word) {
+            const int bb = __ffs(word) - 1;
+            word &= word - 1;
+            tmp[pos++] = (w << 5) + bb;
+          }
+          n_tmp += tot;
+        }
+      }
     }
-    n_tmp += tot;
   }
   *min_v = 0x7fffffff;
   if (n_tmp == 0) return 0;
@@ -617,6 +643,7 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
           }
           if (lane == 0) {
             D.led_st[base + slot] = E_RESERVED;
+            emp_mark(P, D, C, ring, slot, false);
             D.led_g[base + slot] = g;
             D.led_v[base + slot] = vg;
             D.led_b[C.grp_off + g] = b;
@@ -705,8 +732,7 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
     if (g == pass_group) {
       // group versioned in this pass but only partly routed: its other members join the
       // versioned part of the TS
-      for (int m = id + (int)lane; m < (g + 1) * c.G; m += 32)
-        atomicOr(&D.tsv_bits[C.bits_off + (m >> 5)], 1u << (m & 31));
+      for (int m = id + (int)lane; m < (g + 1) * c.G; m += 32) tsv_mark(D, C, m);
       c.vl_head = g + 1;
     } else {
       c.vl_head = g;
@@ -745,7 +771,7 @@ static __device__ int interrupt_victims(const GParams &P, const Dev &D, const Sc
       D.loc[j] = L_TS;
       D.ready[j] = apply_t;
       atomicAdd(&D.n_interrupt[j], 1);
-      atomicOr(&D.tsv_bits[C.bits_off + (id >> 5)], 1u << (id & 31));
+      tsv_mark(D, C, id);
     }
     // one Interrupt record per victim, consecutive commands: lane k's record is the k-th
     const int nk = min(32, nvict - k0);
@@ -891,12 +917,12 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
   const int bw = (P.B + 31) >> 5;
   c.use_bits = nring * bw <= kEmptyWords;
   const int nw = nring * bw;
-  bool e8[8];                                           // empty-slot flags of the first 8 bitmap words
-  const unsigned bw_inv = (65536u + bw - 1) / bw;       // u / bw == (u * bw_inv) >> 16 for u < 8, bw <= 160
+  // the ledger's Empty-slot bitmap (D.led_emp, same word layout as sg.empty): word u * 32 + lane
+  unsigned ew[kEmptyWords / 32];
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const int w = u, r = (int)(((unsigned)w * bw_inv) >> 16), sl = (w - r * bw) * 32 + (int)lane;
-    e8[u] = c.use_bits && w < nw && sl < P.B && D.led_st[C.led_off + (long long)r * P.B + sl] == E_EMPTY;
+  for (int u = 0; u < kEmptyWords / 32; ++u) {
+    const int w = u * 32 + (int)lane;
+    ew[u] = c.use_bits && w < nw ? D.led_emp[(long long)C.ring_off * bw + w] : 0u;
   }
   if (err0) return;
   int consumed_ring = -1;
@@ -934,9 +960,9 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
   if (consumed_ring >= 0) {
     // the consumed ring is now all Empty; Aborted surplus members changed instance fields
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int r = (int)(((unsigned)u * bw_inv) >> 16), sl = (u - r * bw) * 32 + (int)lane;
-      if (r == consumed_ring) e8[u] = c.use_bits && u < nw && sl < P.B;
+    for (int u = 0; u < kEmptyWords / 32; ++u) {
+      const int w = u * 32 + (int)lane;
+      if (w >= consumed_ring * bw && w < (consumed_ring + 1) * bw) ew[u] = ~0u;
     }
     if (P.red && m_aborts > 0) load_w2();
   }
@@ -991,25 +1017,13 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
     }
     if ((int)lane <= C.eta) sfree[lane] = free_l;
     if (c.use_bits) {
-      // ledger empty-slot bitmap: the first 8 words from the loads above, the rest (large
-      // ledgers) 8 words per round with all slot loads issued before their ballots
+      // ledger Empty-slot bitmap into shared memory (loaded above), bits >= B of each ring's last
+      // word cleared (the Reserve search takes the highest set bit)
+      const unsigned tail = (P.B & 31) ? (1u << (P.B & 31)) - 1u : ~0u;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const unsigned m = __ballot_sync(0xffffffffu, e8[u]);
-        if (lane == 0 && u < nw) sg.empty[u] = m;
-      }
-      for (int w0 = 8; w0 < nw; w0 += 8) {
-        bool e[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int w = w0 + u, r = w / bw, sl = (w - r * bw) * 32 + (int)lane;
-          e[u] = w < nw && sl < P.B && D.led_st[C.led_off + (long long)r * P.B + sl] == E_EMPTY;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const unsigned m = __ballot_sync(0xffffffffu, e[u]);
-          if (lane == 0 && w0 + u < nw) sg.empty[w0 + u] = m;
-        }
+      for (int u = 0; u < kEmptyWords / 32; ++u) {
+        const int w = u * 32 + (int)lane;
+        if (w < nw) sg.empty[w] = (w % bw == bw - 1) ? (ew[u] & tail) : ew[u];
       }
     }
     __syncwarp();
@@ -1235,6 +1249,15 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
     }
 #endif
   }
+}
+
+// The coordinator instantiated for scenario s's own instance count, up to the kernel's KS: in a
+// mixed family (C4: I = 8 .. 128) a small scenario does not run the 4-instances-per-lane code.
+template <int KS>
+__device__ __forceinline__ void coord_scenario_fit(const GParams &P, const Dev &D, int s, Stage &sg, const ScenConst C) {
+  if (KS == 1 || C.I <= 32) coord_scenario<1>(P, D, s, sg, C);
+  else if (KS == 2 || C.I <= 64) coord_scenario<KS == 1 ? 1 : 2>(P, D, s, sg, C);
+  else coord_scenario<KS>(P, D, s, sg, C);
 }
 
 }  // namespace sf

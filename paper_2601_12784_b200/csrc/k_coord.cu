@@ -13,7 +13,7 @@ __global__ void __launch_bounds__(32 * kCoordWarps, KS == 1 ? SF_COORD_MINB : 8 
   const ScenConst C = D.sc[s];                     // constant: its load overlaps the wait
   if (P.pdl) warp_wait_geq(&D.f_led[s], P.epoch - 1);   // this scenario's previous window is done
   SF_TRACE_AT(4LL * s);
-  coord_scenario<KS>(P, D, s, stage_all[threadIdx.x >> 5], C);
+  coord_scenario_fit<KS>(P, D, s, stage_all[threadIdx.x >> 5], C);
   SF_TRACE_AT(4LL * s + 1);
   __threadfence();                                 // this lane's writes, device-wide
   __syncwarp();

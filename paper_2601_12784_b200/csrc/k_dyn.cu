@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(32 * kDynWarps, KS == 1 ? 16 / kDynWarps : 8 /
       s = __shfl_sync(0xffffffffu, s, 0);
       if (s < n_scen) {
         SF_TRACE_AT(4LL * s);
-        coord_scenario<KS>(P, D, s, ws.coord, D.sc[s]);
+        coord_scenario_fit<KS>(P, D, s, ws.coord, D.sc[s]);
         SF_TRACE_AT(4LL * s + 1);
         __threadfence();
         __syncwarp();

@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(32 * NW) k_window_block(GParams P, Dev D, int 
   const int w = threadIdx.x >> 5;
   const ScenConst C = D.sc[s];
   for (int win = 0; win < n_windows; ++win) {
-    if (w == 0) coord_scenario<KS>(P, D, s, st0.coord, C);
+    if (w == 0) coord_scenario_fit<KS>(P, D, s, st0.coord, C);
     __syncthreads();
     for (int i = w; i < C.I; i += NW) advance_instance(P, D, C.inst_off + i, adv[w], s, C);
     __syncthreads();

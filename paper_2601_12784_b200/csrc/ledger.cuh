@@ -33,6 +33,23 @@ __device__ __forceinline__ int first_slot(int B, Pred pred) {
   return -1;
 }
 
+// Lowest Empty slot of ring r (-1 if none), from the Empty-slot bitmap: one load per 32 words.
+__device__ __forceinline__ int first_empty(const GParams &P, const Dev &D, const ScenConst &C, int r) {
+  const int bw = (P.B + 31) >> 5;
+  const unsigned *e = D.led_emp + (long long)(C.ring_off + r) * bw;
+  for (int w0 = 0; w0 < bw; w0 += 32) {
+    const int w = w0 + (int)lane_id();
+    unsigned word = w < bw ? e[w] : 0u;
+    if (w == bw - 1 && (P.B & 31)) word &= (1u << (P.B & 31)) - 1u;
+    const unsigned m = __ballot_sync(0xffffffffu, word != 0u);
+    if (m) {
+      const int l = __ffs(m) - 1;
+      return ((w0 + l) << 5) + __ffs(__shfl_sync(0xffffffffu, word, l)) - 1;
+    }
+  }
+  return -1;
+}
+
 // Remove group g's Reserved entry at its ledger position and run the delete-and-relocate
 // cascade (reading A13); (hb, hs) returns the final hole.
 static __device__ void delete_relocate(const GParams &P, const Dev &D, const ScenConst &C, int g, int cu, int &hb,
@@ -47,6 +64,7 @@ static __device__ void delete_relocate(const GParams &P, const Dev &D, const Sce
     __syncwarp();
     if (lane == 0) {
       D.led_st[base + hs] = E_EMPTY; D.led_g[base + hs] = -1; D.led_v[base + hs] = -1;
+      emp_mark(P, D, C, hb % (eta + 1), hs, true);
       D.led_nres[C.ring_off + hb % (eta + 1)] -= 1;
     }
     __syncwarp();
@@ -69,6 +87,8 @@ static __device__ void delete_relocate(const GParams &P, const Dev &D, const Sce
     if (lane == 0) {
       D.led_st[dst] = E_RESERVED; D.led_g[dst] = mg; D.led_v[dst] = mv;
       D.led_st[src] = E_EMPTY; D.led_g[src] = -1; D.led_v[src] = -1;
+      emp_mark(P, D, C, hb % (eta + 1), hs, false);
+      emp_mark(P, D, C, fb % (eta + 1), fs, true);
       D.led_nres[C.ring_off + hb % (eta + 1)] += 1;
       D.led_nres[C.ring_off + fb % (eta + 1)] -= 1;
       D.led_b[C.grp_off + mg] = hb;
@@ -94,8 +114,7 @@ static __device__ void complete_group(const GParams &P, const Dev &D, const Scen
   for (int b = cu; b <= cu + eta; ++b) {
     const int r = C.ring_off + b % (eta + 1);
     if (B - D.led_nres[r] - D.led_nocc[r] <= 0) continue;
-    const long long base = ring_base(C, B, b);
-    os = first_slot(B, [&](int x) { return D.led_st[base + x] == E_EMPTY; });
+    os = first_empty(P, D, C, b % (eta + 1));
     if (os >= 0) { ob = b; break; }
   }
   if (ob < 0) { err = ERR_LEDGER; return; }
@@ -104,6 +123,7 @@ static __device__ void complete_group(const GParams &P, const Dev &D, const Scen
   if (lane == 0) {
     const long long dst = ring_base(C, B, ob) + os;
     D.led_st[dst] = E_OCCUPIED; D.led_g[dst] = g; D.led_v[dst] = vg;
+    emp_mark(P, D, C, ob % (eta + 1), os, false);
     D.led_nocc[C.ring_off + ob % (eta + 1)] += 1;
     D.led_b[C.grp_off + g] = ob;
     D.led_s[C.grp_off + g] = os;
@@ -134,6 +154,8 @@ static __device__ void fill_forward(const GParams &P, const Dev &D, const ScenCo
     if (lane == 0) {
       D.led_st[dst] = E_OCCUPIED; D.led_g[dst] = mg; D.led_v[dst] = mv;
       D.led_st[src] = E_EMPTY; D.led_g[src] = -1; D.led_v[src] = -1;
+      emp_mark(P, D, C, hb % (eta + 1), hs, false);
+      emp_mark(P, D, C, fb % (eta + 1), fs, true);
       D.led_nocc[C.ring_off + hb % (eta + 1)] += 1;
       D.led_nocc[C.ring_off + fb % (eta + 1)] -= 1;
       D.led_b[C.grp_off + mg] = hb;
@@ -162,6 +184,7 @@ static __device__ void filter_group(const GParams &P, const Dev &D, const ScenCo
     __syncwarp();
     if (lane == 0) {
       D.led_st[at] = E_EMPTY; D.led_g[at] = -1; D.led_v[at] = -1;
+      emp_mark(P, D, C, hb % (C.eta + 1), hs, true);
       D.led_nocc[C.ring_off + hb % (C.eta + 1)] -= 1;
     }
     __syncwarp();

@@ -206,7 +206,10 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
   c->hn_pool.assign(ns, 0);
   long long inst = 0, led = 0, ring = 0, list = 0, bits = 0, mlq = 0, ev = 0, batch = 0, cmd = 0;
   const long long pool_traj = (long long)P.pool_cap * G;
-  const long long bwords = (pool_traj + 31) / 32;
+  // TS bitmap words per scenario, padded to whole 32-word chunks (build_mlq reads whole chunks), and
+  // the chunk-summary words (one bit per chunk)
+  const long long bwords = ((pool_traj + 31) / 32 + 31) / 32 * 32;
+  const long long swords = (bwords / 32 + 31) / 32;
   const long long batch_rec = (long long)(P.pool_cap / P.Br + 1) * (1 + 2 * P.Br);
   for (int s = 0; s < ns; ++s) {
     ScenConst &S = c->hsc[s];
@@ -234,6 +237,7 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
     S.inst_off = (int)inst; S.grp_off = s * P.pool_cap; S.led_off = (int)led; S.ring_off = (int)ring;
     S.traj_off = (long long)s * pool_traj; S.list_off = list; S.bits_off = bits; S.mlq_off = mlq;
     S.ev_off = ev; S.batch_off = batch; S.cmd_off = cmd;
+    S.sum_off = (int)(s * swords);
     c->max_inst = std::max(c->max_inst, S.I);
     inst += S.I; led += (long long)(S.eta + 1) * B; ring += S.eta + 1; list += (long long)S.I * S.cap;
     bits += bwords; mlq += 3LL * S.cap + 2; ev += S.cap; batch += batch_rec; cmd += 4LL * P.cmdlog_cap;
@@ -310,6 +314,7 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
   ok = ok && dalloc(c, &D.led_st, led, 0) && dalloc(c, &D.led_g, led, 0xFF) && dalloc(c, &D.led_v, led, 0xFF) &&
        dalloc(c, &D.led_nres, ring, 0) && dalloc(c, &D.led_nocc, ring, 0);
   ok = ok && dalloc(c, &D.ev_t, 1, 0) && dalloc(c, &D.ev_id, ev, 0) && dalloc(c, &D.tsv_bits, bits, 0) &&
+       dalloc(c, &D.tsv_sum, (long long)ns * swords, 0) && dalloc(c, &D.led_emp, ring * ((B + 31) / 32), 0xFF) &&
        dalloc(c, &D.mlq, mlq, 0) && dalloc(c, &D.batches, batch, 0) && dalloc(c, &D.cmdlog, cmd, 0);
   ok = ok && dalloc(c, &c->d_metrics, 2 * sf::kMetrics, 0) && dalloc(c, &c->d_collect, 2 + 2 * P.Br, 0);
   if (!ok) {

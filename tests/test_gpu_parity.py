@@ -114,7 +114,7 @@ def test_single_scenario_presets(name, windows, every, launch_mode):
     run_lockstep(o, g, [0], windows, every=every)
 
 
-def test_c4_subset():
+def test_c4_subset(launch_mode):
     p = W.preset("C4")
     idx = [0, 1, 9, 12, 23, 31, 40, 49]                      # eta 0..4, I 8..128, both pull policies
     o, g = make_pair(p, idx)

@@ -61,6 +61,15 @@ for r in raw[2:]:
         d["achieved_occupancy"] = val(r, "sm__warps_active.avg.pct_of_peak_sustained_active") / 100.0
     if "smsp__warps_eligible.avg.per_cycle_active" in hdr:
         d["eligible_warps_per_sched"] = val(r, "smsp__warps_eligible.avg.per_cycle_active")
+    # stall breakdown: warp cycles per issued instruction spent in each stall reason (the CPI stack)
+    st = {}
+    for i, hname in enumerate(hdr):
+        if hname.startswith("smsp__average_warps_issue_stalled_") and hname.endswith("_per_issue_active.ratio"):
+            try:
+                st[hname[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]] = float(r[i])
+            except ValueError:
+                pass
+    d["stall_cycles_per_issue"] = dict(sorted(st.items(), key=lambda kv: -kv[1])[:10])
     out[name] = d
 json.dump({"source": "ncu --set full, window 181 of the C5 workload (tools/profile_round.sh)", "kernels": out},
           open(os.path.join(dst, "ncu_kernels.json"), "w"), indent=1)
