@@ -48,36 +48,112 @@ void sf_launch_window_fused(const sf::GParams &P, const sf::Dev &D, int n_scen, 
 }
 
 // ---------------------------------------------------------------------------------------------
-// Block-per-scenario window kernel (SF_LAUNCH=block; the default for contexts with few scenarios,
-// sf_api.cu): one block runs one scenario through all n_windows windows of the call -- warp 0 the
-// coordinator (W0-W5), then every warp advances a share of the scenario's instances in parallel
-// (W6-W7), then warp 0 the reward ledger (W8-W9) -- with __syncthreads() between the phases instead
-// of kernel boundaries.  A single scenario (C1-C3) is one latency-bound chain per window, so the
-// three launches and their hand-offs per window are what this removes.
+// Block mode (SF_LAUNCH=block; the default for contexts with few scenarios, sf_api.cu): one block
+// -- or one thread-block cluster for a scenario with many instances -- runs one scenario through all
+// n_windows windows of the call: warp 0 the coordinator (W0-W5), then every warp advances a share of
+// the scenario's instances in parallel (W6-W7), then warp 0 the reward ledger (W8-W9), with
+// barriers between the phases instead of kernel boundaries.  A single scenario (C1-C3) is one
+// latency-bound chain per window, so the three launches and their hand-offs per window are what
+// this removes.
 namespace sf {
 
-template <int KS, int NW>
-__global__ void __launch_bounds__(32 * NW) k_window_block(GParams P, Dev D, int n_windows) {
+__device__ __forceinline__ unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_idx() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+// every thread of every CTA of the cluster; release / acquire at cluster scope orders the global
+// writes of one phase before the reads of the next (all global loads are L2 loads, -dlcm=cg)
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Cluster-per-scenario window kernel (block mode for scenarios with many instances): the CL CTAs
+// of cluster k run scenario list[k] through all n_windows windows -- CTA 0's warp 0 the coordinator
+// and the ledger, all CL * NW warps the advance of the scenario's instances (warp r * NW + w takes
+// instances r * NW + w, + CL * NW, ...) -- with cluster barriers between the phases.  A large
+// scenario's advance (I = 128: 16 instances per warp in one block) spreads over CL SMs.  CL = 1 is
+// the plain block kernel over a scenario list.  Two barriers per window suffice: the ledger of window
+// w and the coordinator of w + 1 run on the same warp, in order.
+template <int KS, int NW, int CL>
+__global__ void __launch_bounds__(32 * NW) k_window_cluster(GParams P, Dev D, const int *list, int n_windows) {
   __shared__ union { Stage coord; EvStage led; } st0;
   __shared__ AdvStage adv[NW];
-  const int s = blockIdx.x;
+  const int rank = CL > 1 ? (int)cluster_ctarank() : 0;
+  const int s = list[CL > 1 ? (int)cluster_idx() : (int)blockIdx.x];
   const int w = threadIdx.x >> 5;
   const ScenConst C = D.sc[s];
   for (int win = 0; win < n_windows; ++win) {
-    if (w == 0) coord_scenario_fit<KS>(P, D, s, st0.coord, C);
-    __syncthreads();
-    for (int i = w; i < C.I; i += NW) advance_instance(P, D, C.inst_off + i, adv[w], s, C);
-    __syncthreads();
-    if (w == 0) ledger_scenario(P, D, s, st0.led, C);
-    __syncthreads();
-  }
+    if (rank == 0 && w == 0) coord_scenario_fit<KS>(P, D, s, st0.coord, C);
+    if constexpr (CL > 1) cluster_barrier(); else __syncthreads();
+    for (int i = rank * NW + w; i < C.I; i += CL * NW) advance_instance(P, D, C.inst_off + i, adv[w], s, C);
+    if constexpr (CL > 1) cluster_barrier(); else __syncthreads();
+    if (rank == 0 && w == 0) ledger_scenario(P, D, s, st0.led, C);
+    if constexpr (CL == 1) __syncthreads();     // not needed for ordering; keeps ptxas' 128-register
+  }                                             // allocation of the 16-warp variant at its smallest spill
 }
 
 }  // namespace sf
 
-void sf_launch_window_block(const sf::GParams &P, const sf::Dev &D, int n_scen, int max_inst, int n_windows,
-                            cudaStream_t st) {
-  if (max_inst <= 32) sf::k_window_block<1, 16><<<n_scen, 32 * 16, 0, st>>>(P, D, n_windows);
-  else if (max_inst <= 64) sf::k_window_block<2, 8><<<n_scen, 32 * 8, 0, st>>>(P, D, n_windows);
-  else sf::k_window_block<4, 8><<<n_scen, 32 * 8, 0, st>>>(P, D, n_windows);
+
+template <int KS, int NW, int CL>
+static cudaError_t launch_cluster(const sf::GParams &P, const sf::Dev &D, const int *list, int n, int n_windows,
+                                  cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(n * CL));
+  cfg.blockDim = dim3(32 * NW);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = CL > 1 ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, sf::k_window_cluster<KS, NW, CL>, P, D, list, n_windows);
+}
+
+// One scenario class of the block mode (sf_api.cu): ks instances per coordinator lane, cl CTAs per
+// scenario.  Returns cudaErrorInvalidValue for an unsupported pair.
+cudaError_t sf_launch_window_cluster(const sf::GParams &P, const sf::Dev &D, const int *list, int n, int ks, int cl,
+                                     int n_windows, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  if (ks == 1 && cl == 1) return launch_cluster<1, 16, 1>(P, D, list, n, n_windows, st);
+  if (ks == 1 && cl == 2) return launch_cluster<1, 8, 2>(P, D, list, n, n_windows, st);
+  if (ks == 2 && cl == 1) return launch_cluster<2, 8, 1>(P, D, list, n, n_windows, st);
+  if (ks == 2 && cl == 2) return launch_cluster<2, 8, 2>(P, D, list, n, n_windows, st);
+  if (ks == 2 && cl == 4) return launch_cluster<2, 8, 4>(P, D, list, n, n_windows, st);
+  if (ks == 4 && cl == 1) return launch_cluster<4, 8, 1>(P, D, list, n, n_windows, st);
+  if (ks == 4 && cl == 2) return launch_cluster<4, 8, 2>(P, D, list, n, n_windows, st);
+  if (ks == 4 && cl == 4) return launch_cluster<4, 8, 4>(P, D, list, n, n_windows, st);
+  if (ks == 4 && cl == 8) return launch_cluster<4, 8, 8>(P, D, list, n, n_windows, st);
+  return cudaErrorInvalidValue;
+}
+
+// Largest number of co-resident clusters of cl CTAs of the (ks, cl) kernel (cudaOccupancyMaxActiveClusters).
+int sf_max_active_clusters(int ks, int cl) {
+  cudaLaunchConfig_t cfg = {};
+  const int nw = ks == 1 && cl == 1 ? 16 : 8;
+  cfg.gridDim = dim3((unsigned)(cl * 64));
+  cfg.blockDim = dim3(32 * nw);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  cudaError_t e = cudaErrorInvalidValue;
+  if (ks == 4 && cl == 8) e = cudaOccupancyMaxActiveClusters(&n, sf::k_window_cluster<4, 8, 8>, &cfg);
+  else if (ks == 4 && cl == 4) e = cudaOccupancyMaxActiveClusters(&n, sf::k_window_cluster<4, 8, 4>, &cfg);
+  else if (ks == 2 && cl == 4) e = cudaOccupancyMaxActiveClusters(&n, sf::k_window_cluster<2, 8, 4>, &cfg);
+  else if (ks == 2 && cl == 2) e = cudaOccupancyMaxActiveClusters(&n, sf::k_window_cluster<2, 8, 2>, &cfg);
+  return e == cudaSuccess ? n : 0;
 }

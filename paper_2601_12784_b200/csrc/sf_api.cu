@@ -27,7 +27,15 @@ struct sf_ctx {
   int n_inst_total = 0;
   int max_inst = 1;
   int fused = 0;                      // launch mode: 1 = one fused window kernel (k_window)
-  int block = 0;                      // launch mode: one block per scenario for the whole call (k_window_block)
+  int block = 0;                      // launch mode: one block (or cluster) per scenario for the whole call
+  struct BlockClass {                 // block mode: scenarios of one instance-count class (k_window_cluster)
+    int ks = 1, cl = 1, n = 0, off = 0;
+    cudaStream_t st = nullptr;        // classes after the first run on their own stream (fork / join)
+    cudaEvent_t ev = nullptr;
+  } bc[3];
+  std::vector<int> hblist;            // scenario indices, class by class (device copy d_blist)
+  int *d_blist = nullptr;
+  cudaEvent_t ev_fork = nullptr;
   int pdl = 1;                        // programmatic dependent launch between window kernels
   int lanes = 0;                      // split mode: one-lane-per-instance advance kernel (SF_ADVANCE=lanes)
   int pdl_mask = 0;                   // debugging (SF_PDL_MASK): bit 0 serializes the advance, bit 1 the ledger
@@ -265,13 +273,32 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
     c->P.skip = strcmp(m, "step") != 0;
     c->lanes = strcmp(m, "lanes") == 0;
   }
-  // few scenarios (at most one per SM): one block per scenario for the whole call (k_window_block,
-  // the window's phases separated by __syncthreads instead of kernel launches); many scenarios: the
-  // three-kernel split with programmatic dependent launch (measured)
+  // few scenarios: one block per scenario for the whole call (k_window_cluster, the window's phases
+  // separated by barriers instead of kernel launches) -- a 16-warp block for I <= 32, a cluster of 2
+  // blocks for 32 < I <= 64, of 4 (8 when the GPU holds them all at once) for I > 64, so that a
+  // large scenario's advance spreads over several SMs; used when every block has an SM of its own.
+  // Many scenarios: the three-kernel split with programmatic dependent launch.
+  // SF_CLUSTER=1 runs every class without clusters, SF_CLUSTER=4 / 8 fixes the I > 64 cluster.
   {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device);
-    c->block = ns <= sms;
+    std::vector<int> cls[3];
+    for (int s = 0; s < ns; ++s) cls[c->hsc[s].I <= 32 ? 0 : c->hsc[s].I <= 64 ? 1 : 2].push_back(s);
+    int clB = 2, clC = 4;
+    const char *ce = getenv("SF_CLUSTER");
+    if (ce && atoi(ce) == 1) clB = clC = 1;
+    if (ce && (atoi(ce) == 4 || atoi(ce) == 8)) clC = atoi(ce);
+    const long long nA = (long long)cls[0].size(), nB = (long long)cls[1].size(), nC = (long long)cls[2].size();
+    if (!ce && nC > 0 && nA + clB * nB + 8 * nC <= sms && sf_max_active_clusters(4, 8) >= nC) clC = 8;
+    c->block = nA + clB * nB + clC * nC <= sms;
+    const int ks[3] = {1, 2, 4}, cl[3] = {1, clB, clC};
+    for (int k = 0; k < 3; ++k) {
+      c->bc[k].ks = ks[k];
+      c->bc[k].cl = cl[k];
+      c->bc[k].n = (int)cls[k].size();
+      c->bc[k].off = (int)c->hblist.size();
+      c->hblist.insert(c->hblist.end(), cls[k].begin(), cls[k].end());
+    }
   }
   if (const char *m = getenv("SF_LAUNCH")) {
     if (!strcmp(m, "split")) { c->fused = 0; c->dyn = 0; c->block = 0; }
@@ -285,7 +312,8 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
   ScenConst *dsc = nullptr;
   ScenState *dss = nullptr;
   int *dinst_scen = nullptr;
-  ok = ok && dalloc(c, &dsc, ns, 0) && dalloc(c, &dss, ns, 0) && dalloc(c, &dinst_scen, inst, 0);
+  ok = ok && dalloc(c, &dsc, ns, 0) && dalloc(c, &dss, ns, 0) && dalloc(c, &dinst_scen, inst, 0) &&
+       dalloc(c, &c->d_blist, ns, 0);
   ok = ok && dalloc(c, &D.T, ntraj, 0) && dalloc(c, &D.gen, ntraj, 0) && dalloc(c, &D.loc, ntraj, 0) &&
        dalloc(c, &D.tinst, ntraj, 0xFF) && dalloc(c, &D.n_routes, ntraj, 0) && dalloc(c, &D.n_preempt, ntraj, 0) &&
        dalloc(c, &D.n_interrupt, ntraj, 0) && dalloc(c, &D.t_complete, ntraj, 0xFF) && dalloc(c, &D.ready, ntraj, 0);
@@ -343,7 +371,15 @@ sf_status sf_create(int32_t instances, int32_t eta, int32_t group_size, const sf
   bool cp = cudaMemcpyAsync(dsc, c->hsc.data(), sizeof(ScenConst) * ns, cudaMemcpyHostToDevice, c->stream) == cudaSuccess &&
             cudaMemcpyAsync(dss, hss.data(), sizeof(ScenState) * ns, cudaMemcpyHostToDevice, c->stream) == cudaSuccess &&
             cudaMemcpyAsync(dinst_scen, hinst_scen.data(), sizeof(int) * inst, cudaMemcpyHostToDevice, c->stream) == cudaSuccess &&
+            cudaMemcpyAsync(c->d_blist, c->hblist.data(), sizeof(int) * ns, cudaMemcpyHostToDevice, c->stream) == cudaSuccess &&
             cudaStreamSynchronize(c->stream) == cudaSuccess;
+  // block mode with several classes: one stream and event per class after the first (fork / join)
+  if (cp && c->block && (c->bc[0].n > 0) + (c->bc[1].n > 0) + (c->bc[2].n > 0) > 1) {
+    cp = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) == cudaSuccess;
+    for (int k = 0; k < 3 && cp; ++k)
+      cp = cudaStreamCreateWithFlags(&c->bc[k].st, cudaStreamNonBlocking) == cudaSuccess &&
+           cudaEventCreateWithFlags(&c->bc[k].ev, cudaEventDisableTiming) == cudaSuccess;
+  }
   if (!cp) {
     sf_destroy(c);
     return SF_E_CUDA;
@@ -362,6 +398,11 @@ void sf_destroy(sf_ctx *c) {
   if (c->d_dump) cudaFree(c->d_dump);
   if (c->h_desc) cudaFreeHost(c->h_desc);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  for (auto &b : c->bc) {
+    if (b.st) { cudaStreamSynchronize(b.st); cudaStreamDestroy(b.st); }
+    if (b.ev) cudaEventDestroy(b.ev);
+  }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   delete c;
 }
 
@@ -444,6 +485,32 @@ sf_status sf_submit_prompts(sf_ctx *c, int32_t scenario, int32_t n_groups, const
   return sf_submit_prompts_many(c, 1, &scenario, &n_groups, prompt_len, target_len);
 }
 
+// Block mode: one launch per non-empty scenario class; the first on the context stream, the others
+// forked onto the class streams after the stream's prior work and joined back before what follows.
+static cudaError_t launch_block_classes(sf_ctx *c, int n_windows) {
+  cudaError_t e = cudaSuccess;
+  const bool fork = c->ev_fork != nullptr;
+  if (fork && (e = cudaEventRecord(c->ev_fork, c->stream)) != cudaSuccess) return e;
+  bool main_used = false;
+  for (auto &b : c->bc) {
+    if (b.n == 0) continue;
+    cudaStream_t st = c->stream;
+    if (main_used) {
+      st = b.st;
+      if ((e = cudaStreamWaitEvent(st, c->ev_fork, 0)) != cudaSuccess) return e;
+    }
+    if ((e = sf_launch_window_cluster(c->P, c->D, c->d_blist + b.off, b.n, b.ks, b.cl, n_windows, st)) != cudaSuccess)
+      return e;
+    c->launches += 1;
+    if (main_used) {
+      if ((e = cudaEventRecord(b.ev, st)) != cudaSuccess) return e;
+      if ((e = cudaStreamWaitEvent(c->stream, b.ev, 0)) != cudaSuccess) return e;
+    }
+    main_used = true;
+  }
+  return e;
+}
+
 sf_status sf_step(sf_ctx *c, int32_t n_windows, sf_step_stats *out) {
   sf_status st = check_ctx(c);
   if (st != SF_OK) return st;
@@ -462,9 +529,8 @@ sf_status sf_step(sf_ctx *c, int32_t n_windows, sf_step_stats *out) {
   }
   if (c->block && !c->fused && n_windows > 0) {
     prof_mark(c, 3);
-    sf_launch_window_block(c->P, c->D, c->n_scen, c->max_inst, n_windows, c->stream);
+    if (!cuda_ok(c, launch_block_classes(c, n_windows), "block launch")) return SF_E_CUDA;
     prof_mark(c, 3);
-    c->launches += 1;
   }
   // Split mode: three kernels per window.  With PDL each kernel may start while its predecessor
   // runs and waits per scenario on the progress flags (epoch = split windows so far), so a
