@@ -197,6 +197,42 @@ static __device__ int build_mlq(const GParams &P, const Dev &D, const ScenConst 
 }
 
 
+// The waterfall's reduction (route_pass): over the lanes' best (key = version << 7 | instance, d),
+// key 0x7fffffff = none, the lowest version, then the highest d, then the lowest instance; returns
+// that key in every lane (0x7fffffff: no candidate).  For wide warps (>= SF_REDUX_MIN lanes hold
+// instances) four single-instruction redux.sync reductions: the version, then the two halves of d's
+// order-preserving bit pattern among the lanes still in, then the key; narrow ones butterfly
+// shuffles over red_w lanes.  d is never -0.0 (a difference of two positive T values, or 0.0), so
+// the bit-pattern order is the double order.
+#ifndef SF_REDUX_MIN
+#define SF_REDUX_MIN 8
+#endif
+__device__ __forceinline__ int waterfall_reduce(int bk, double bd, int red_w) {
+  if (red_w >= SF_REDUX_MIN) {
+    const unsigned vk = (unsigned)bk >> 7;
+    const unsigned vmin = __reduce_min_sync(0xffffffffu, vk);
+    if (vmin == (0x7fffffffu >> 7)) return 0x7fffffff;
+    const unsigned long long b = (unsigned long long)__double_as_longlong(bd);
+    const unsigned long long u = (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+    bool in = vk == vmin;
+    const unsigned hmax = __reduce_max_sync(0xffffffffu, in ? (unsigned)(u >> 32) : 0u);
+    in = in && (unsigned)(u >> 32) == hmax;
+    const unsigned lmax = __reduce_max_sync(0xffffffffu, in ? (unsigned)u : 0u);
+    in = in && (unsigned)u == lmax;
+    return (int)__reduce_min_sync(0xffffffffu, in ? (unsigned)bk : 0xffffffffu);
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    if (o >= red_w) break;
+    const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+    const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+    const bool better = ((ok >> 7) < (bk >> 7)) | (((ok >> 7) == (bk >> 7)) & ((od > bd) | ((od == bd) & (ok < bk))));
+    bk = better ? ok : bk;
+    bd = better ? od : bd;
+  }
+  return __shfl_sync(0xffffffffu, bk, 0);
+}
+
 // Group-batched routing (one instance per lane, KS == 1).  After the first member of a
 // versionless group is routed (which fixed v_g and Reserved), its remaining members are the next
 // MLQ items (consecutive ids, same l = p since gen = 0, same candidate set {i : S[i].v >= v_g},
@@ -267,18 +303,7 @@ static __device__ int route_group_batch(const GParams &P, const Dev &D, const Sc
     // waterfall as one reduction (see route_pass): lowest version with dT >= thr, then highest dT,
     // then lowest id
     int sel = -1;
-    int bk = (cnd && my >= thr) ? ((S.v[0] << 7) | (int)lane) : 0x7fffffff;
-    double bd = my;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      if (o >= c.red_w) break;
-      const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
-      const double od = __shfl_xor_sync(0xffffffffu, bd, o);
-      const bool better = ((ok >> 7) < (bk >> 7)) | (((ok >> 7) == (bk >> 7)) & ((od > bd) | ((od == bd) & (ok < bk))));
-      bk = better ? ok : bk;
-      bd = better ? od : bd;
-    }
-    bk = __shfl_sync(0xffffffffu, bk, 0);
+    const int bk = waterfall_reduce((cnd && my >= thr) ? ((S.v[0] << 7) | (int)lane) : 0x7fffffff, my, c.red_w);
     if (bk != 0x7fffffff) sel = bk & 127;
     if (sel < 0) { stopped = true; break; }
     if (tentative >= 0 && sel == tentative) { hit = true; return done + 1; }
@@ -564,13 +589,14 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
         for (int q = 0; q < KS; ++q) {
           Tn[q] = 0.0;
           double d = 0.0;
-          if (cand[q] && S.w[q] == 0 && S.kv[q] + (long long)P.k5 * l <= P.M) {      // gamma (Eq 3)
-#ifdef SF_AB_NODIV
-            Tn[q] = (double)(S.n[q] + 1) * 1e-9 - (double)(S.kv[q] + (long long)P.k5 * l) * 1e-15;  // timing A/B only
-#else
-            Tn[q] = throughput_d(P, S.n[q] + 1, S.kv[q] + (long long)P.k5 * l);
-#endif
-            d = __dsub_rn(Tn[q], Tcur[q]);
+          {
+            // gamma (Eq 3); the division is issued for every owned instance (branch-free, the KS
+            // divisions overlap) and its result kept only where gamma holds.  kv + k5 l <= M < 2^31.
+            const long long kvl = S.kv[q] + (long long)P.k5 * l;
+            const bool gam = cand[q] & (S.w[q] == 0) & (kvl <= P.M);
+            const double t = throughput_nz(P, S.n[q] + 1, gam ? (int)kvl : 0);
+            Tn[q] = gam ? t : 0.0;
+            d = gam ? __dsub_rn(t, Tcur[q]) : 0.0;
           }
           const int key = (S.v[q] << 7) | ((int)lane + 32 * q);
           // branch-free (bitwise predicates + selects): data-dependent short-circuit branches
@@ -579,18 +605,7 @@ __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cy
           bk = take ? key : bk;
           bd = take ? d : bd;
         }
-#ifndef SF_AB_NORED
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          if (o >= c.red_w) break;
-          const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
-          const double od = __shfl_xor_sync(0xffffffffu, bd, o);
-          const bool better = ((ok >> 7) < (bk >> 7)) | (((ok >> 7) == (bk >> 7)) & ((od > bd) | ((od == bd) & (ok < bk))));
-          bk = better ? ok : bk;
-          bd = better ? od : bd;
-        }
-#endif
-        bk = __shfl_sync(0xffffffffu, bk, 0);
+        bk = waterfall_reduce(bk, bd, c.red_w);
         if (bk != 0x7fffffff) sel = bk & 127;               // accept (reading A4)
       }
       SF_RT(2);
