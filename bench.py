@@ -360,7 +360,7 @@ def main():
     traffic = kn.get(kname, {}).get("dram_bytes_per_launch")
     share = {KERNELS[i]: float(kern_ms[i] / max(1e-9, kern_ms.sum())) for i in range(4) if kern_n[i]}
     issue = {k: {"issue_active_frac": v.get("issue_active_frac"), "warps_per_sched": v.get("eligible_warps_per_sched"),
-                 "achieved_occupancy": v.get("achieved_occupancy")} for k, v in kn.items()} or None
+                 "achieved_occupancy": v.get("achieved_occupancy")} for k, v in kn.items() if k in share} or None
 
     # ---------------- e2e: the same complete runs through the C ABI with host buffers: per step the
     # pool's H2D from pinned memory (sf_submit_prompts_many), every window, the metrics' D2H
@@ -430,8 +430,10 @@ def main():
                          "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                          "algorithmic_bytes_per_traj_iter": ALGO_BYTES_PER_ITER,
                          "launches": int(kern_n[kid]), "ms_per_launch": ms_per_launch, "step_share": share,
-                         "timing": "CUDA events around every launch in a serialized replay of one step "
-                                   "(same inputs and work; the timed steps overlap kernels via PDL)",
+                         "timing": ("CUDA events around every launch in a serialized replay of one step "
+                                    "(same inputs and work; the timed steps overlap kernels via PDL)") if kname != "k_window"
+                                   else ("CUDA events around every window-kernel launch (block / cluster mode: one "
+                                         "launch per sf_step call runs all its windows) in a replay of one step"),
                          "issue_slots_ncu": issue, "ncu_source": os.path.relpath(NCU_FILE, ROOT) if ncu else None},
             "cpu_baseline": cpu,
             "e2e": e2e,

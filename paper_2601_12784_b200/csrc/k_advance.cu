@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, SF_ADV_MINB) k_advance(GP
   SF_TRACE_AT(4LL * P.n_scen + 2LL * gi);
   advance_instance(P, D, gi, stage_all[threadIdx.x >> 5], s, C, &pre);
   SF_TRACE_AT(4LL * P.n_scen + 2LL * gi + 1);
-  __threadfence();                                 // this lane's writes, device-wide
+  fence_release();                                 // this lane's writes, device-wide
   __syncwarp();
   if ((threadIdx.x & 31) == 0) add_release(&D.f_adv[s], 1);
 }

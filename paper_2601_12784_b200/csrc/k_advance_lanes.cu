@@ -17,7 +17,7 @@ __global__ void __launch_bounds__(32) k_advance_lanes(GParams P, Dev D, int n_in
   advance_lanes(P, D, gi0, n_inst_total, sm.lanes, sm.stage);
   // per instance: its writes, then the scenario's count of finished advances (release)
   const int gi = gi0 + (int)threadIdx.x;
-  __threadfence();
+  fence_release();                                 // this lane's writes, device-wide
   __syncwarp();
   if ((int)threadIdx.x < kLanes && gi < n_inst_total) add_release(&D.f_adv[D.inst_scen[gi]], 1);
 }

@@ -15,7 +15,7 @@ __global__ void __launch_bounds__(32 * kCoordWarps, KS == 1 ? SF_COORD_MINB : 8 
   SF_TRACE_AT(4LL * s);
   coord_scenario_fit<KS>(P, D, s, stage_all[threadIdx.x >> 5], C);
   SF_TRACE_AT(4LL * s + 1);
-  __threadfence();                                 // this lane's writes, device-wide
+  fence_release();                                 // this lane's writes, device-wide
   __syncwarp();
   if ((threadIdx.x & 31) == 0) st_release(&D.f_coord[s], P.epoch);
 }

@@ -14,7 +14,7 @@ __global__ void __launch_bounds__(32 * kLedgerWarps) k_ledger(GParams P, Dev D) 
   SF_TRACE_AT(4LL * s + 2);
   ledger_scenario(P, D, s, stage_all[threadIdx.x >> 5], C);
   SF_TRACE_AT(4LL * s + 3);
-  __threadfence();                                 // this lane's writes, device-wide
+  fence_release();                                 // this lane's writes, device-wide
   __syncwarp();
   if ((threadIdx.x & 31) == 0) st_release(&D.f_led[s], P.epoch);
 }
