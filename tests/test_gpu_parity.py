@@ -19,11 +19,11 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(params=["auto", "split", "lanes", "fused", "block", "step", "dyn", "nopdl"])
 def launch_mode(request, monkeypatch):
     """Every launch / decode-step mode must give identical results: the default (a block per
-    scenario for contexts with at most one scenario per SM, else the split), the split (three
-    kernels with programmatic dependent launch, one warp per instance and closed-form quiet steps
-    in the advance), the one-lane-per-instance advance, the fused window kernel, the
-    block-per-scenario window kernel, one-by-one decode steps, the dataflow window kernel, and three
-    fully serialized kernels."""
+    scenario -- a thread-block cluster for many instances -- when every block gets an SM, else the
+    split), the split (three kernels with programmatic dependent launch, one warp per instance and
+    closed-form quiet steps in the advance), the one-lane-per-instance advance, the fused window
+    kernel, the block / cluster-per-scenario window kernel, one-by-one decode steps, the dataflow
+    window kernel, and three fully serialized kernels."""
     monkeypatch.delenv("SF_LAUNCH", raising=False)
     monkeypatch.delenv("SF_ADVANCE", raising=False)
     monkeypatch.delenv("SF_PDL", raising=False)
