@@ -81,13 +81,12 @@ __device__ __forceinline__ bool verify_free(const int *sfree, int v, int cu, int
 // verify(v) for every v = cu - eta + d, d in [0, eta], as a bitmask: bit d is set iff one of
 // the buffers cu .. cu + d has a free slot (the reserve range [max(v, cu), v + eta] = [cu, cu+d]).
 // Versions below cu - eta can never verify.
+// One ballot (all lanes): bit d of the result is set from the lowest d with a free slot up to eta.
 __device__ __forceinline__ unsigned verify_mask(const int *sfree, int eta) {
-  unsigned m = 0, any = 0;
-  for (int d = 0; d <= eta; ++d) {
-    any |= sfree[d] > 0;
-    m |= any << d;
-  }
-  return m;
+  const int lane = (int)lane_id();
+  const unsigned m = __ballot_sync(0xffffffffu, lane <= eta && sfree[lane] > 0);
+  const unsigned low = m & (0u - m);
+  return low ? (((2u << eta) - 1u) & ~(low - 1u)) : 0u;
 }
 
 __device__ __forceinline__ void log_cmd(const GParams &P, const Dev &D, const ScenConst &C, Cyc &c, int kind,
@@ -170,27 +169,28 @@ static __device__ int build_mlq(const GParams &P, const Dev &D, const ScenConst 
   }
   __syncwarp();
   if (__any_sync(0xffffffffu, bad)) { *min_v = -1; return 0; }
-  int base[kMaxEta + 1];
-  int acc = 0;
-#pragma unroll
-  for (int d = 0; d <= kMaxEta; ++d) {
-    base[d] = acc;
-    if (d < nv) {
-      if (sg.vcnt[d] > 0 && *min_v == 0x7fffffff) *min_v = vlo + d;
-      acc += sg.vcnt[d];
-    }
+  {
+    // bucket bases: exclusive prefix of the counts over d < nv (nv <= kMaxEta + 1 <= 32), in place;
+    // the smallest version present
+    const int cnt = (int)lane < nv ? sg.vcnt[lane] : 0;
+    const int ex = warp_excl_scan(cnt);
+    const unsigned nz = __ballot_sync(0xffffffffu, cnt > 0);
+    if (nz) *min_v = vlo + __ffs(nz) - 1;
+    __syncwarp();
+    if ((int)lane < nv) sg.vcnt[lane] = ex;
+    __syncwarp();
   }
   for (int k0 = 0; k0 < n_tmp; k0 += 32) {
+    // stable scatter: rank among the chunk's lanes with the same bucket, then each bucket's base
+    // advances by its count (added by the bucket's highest lane)
     const int k = k0 + (int)lane;
     const int key = k < n_tmp ? tmp[k] : -1;
     const int dk = key >= 0 ? (key >> 27) : -1;
-#pragma unroll
-    for (int d = 0; d <= kMaxEta; ++d) {
-      if (d >= nv) break;
-      const unsigned m = __ballot_sync(0xffffffffu, dk == d);
-      if (dk == d) out[base[d] + __popc(m & lanemask_lt())] = key & 0x7ffffff;
-      base[d] += __popc(m);
-    }
+    const unsigned same = __match_any_sync(0xffffffffu, dk);
+    if (dk >= 0) out[sg.vcnt[dk] + __popc(same & lanemask_lt())] = key & 0x7ffffff;
+    __syncwarp();
+    if (dk >= 0 && (same >> lane) == 1u) sg.vcnt[dk] += __popc(same);
+    __syncwarp();
   }
   __syncwarp();
   return n_tmp;
@@ -254,7 +254,7 @@ static __device__ int route_group_batch(const GParams &P, const Dev &D, const Sc
     // other (branch-free div_int_rn), so they are issued together.
     const bool ok0 = cnd && S.w[0] == 0;
     double prev = Tcur;
-#pragma unroll
+#pragma unroll 4
     for (int j = 0; j < kGMax; ++j) {
       if (j >= nrem) break;
       const long long kvj = S.kv[0] + (long long)(j + 1) * k5l;
