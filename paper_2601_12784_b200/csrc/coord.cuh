@@ -115,6 +115,7 @@ static __device__ int build_mlq(const GParams &P, const Dev &D, const ScenConst 
   // found all-zero has its summary bit cleared (bits are set only by tsv_mark)
   if (w_lo < w_hi) {
     const int c_lo = w_lo >> 5, c_hi = (w_hi - 1) >> 5;          // chunks [c_lo, c_hi]
+#pragma unroll 1
     for (int s0 = c_lo >> 5; s0 <= (c_hi >> 5); s0 += 32) {
       const int sw = s0 + (int)lane;
       unsigned sm = sw <= (c_hi >> 5) ? D.tsv_sum[C.sum_off + sw] : 0u;
@@ -158,6 +159,7 @@ static __device__ int build_mlq(const GParams &P, const Dev &D, const ScenConst 
   if ((int)lane < kMaxEta + 2) sg.vcnt[lane] = 0;
   __syncwarp();
   bool bad = false;
+#pragma unroll 1
   for (int k0 = 0; k0 < n_tmp; k0 += 32) {
     const int k = k0 + (int)lane;
     if (k < n_tmp) {
@@ -180,6 +182,7 @@ static __device__ int build_mlq(const GParams &P, const Dev &D, const ScenConst 
     if ((int)lane < nv) sg.vcnt[lane] = ex;
     __syncwarp();
   }
+#pragma unroll 1
   for (int k0 = 0; k0 < n_tmp; k0 += 32) {
     // stable scatter: rank among the chunk's lanes with the same bucket, then each bucket's base
     // advances by its count (added by the bucket's highest lane)
