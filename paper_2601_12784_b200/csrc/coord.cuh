@@ -478,9 +478,13 @@ static __device__ int route_versioned_rep(const GParams &P, const Dev &D, const 
 // [versionless groups vl_head..n_ingested).  tentative >= 0: Alg 3 trial for that instance on
 // scratch state, returns 1 as soon as a route targets it (early exit allowed).
 // Otherwise issues Route commands and Reserves on the live ledger; returns routes issued.
-template <int KS>
+// TRIAL (compile time): an Alg 3 trial (tentative_in >= 0) or the real pass (tentative_in ignored,
+// -1): each instantiation drops the other's code -- the trial all writes, the pass the early exits.
+template <int KS, bool TRIAL>
 __device__ int route_pass(const GParams &P, const Dev &D, const ScenConst &C, Cyc &c, InstRegs<KS> &S,
-                          int *sfree, int acc_delta[KS], int arrn[KS], Stage &sg, bool vanilla, int tentative) {
+                          int *sfree, int acc_delta[KS], int arrn[KS], Stage &sg, bool vanilla, int tentative_in) {
+  const int tentative = TRIAL ? tentative_in : -1;
+  if (TRIAL) __builtin_assume(tentative >= 0);
   const unsigned lane = lane_id();
   const int total = c.n_v + c.n_vl;
   int pass_group = -1, pass_vg = -1, routed = 0;
@@ -1083,7 +1087,7 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
           for (int qq = 0; qq < KS; ++qq) { dummy_a[qq] = 0; dummy_b[qq] = 0; }
           Cyc ct = c;
           ++dbg_tent;
-          if (route_pass<KS>(P, D, C, ct, T, sg.sfree_tmp, dummy_a, dummy_b, sg, vanilla_route, i)) keep |= 1u << li;
+          if (route_pass<KS, true>(P, D, C, ct, T, sg.sfree_tmp, dummy_a, dummy_b, sg, vanilla_route, i)) keep |= 1u << li;
         }
         selmask[q] = keep;
       }
@@ -1198,7 +1202,7 @@ __device__ __forceinline__ void coord_scenario(const GParams &P, const Dev &D, i
 #ifdef SF_TIMING
     const long long t_rp = clock64();
 #endif
-    const int nr = route_pass<KS>(P, D, C, c, S, sfree, acc_delta, arrn, sg, vanilla_route, -1);
+    const int nr = route_pass<KS, false>(P, D, C, c, S, sfree, acc_delta, arrn, sg, vanilla_route, -1);
 #ifdef SF_TIMING
     dbg_tent = (int)(clock64() - t_rp);          // (slot 7) cycles in the real routing pass
 #endif
